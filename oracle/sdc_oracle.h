@@ -1,0 +1,56 @@
+/*
+ * sdc_oracle.h -- declarations of the CPU fp64 ORACLE (test infrastructure only).
+ * Independent of include/sdc.h: the oracle keeps its own constants and result struct.
+ * All matrices are host memory, column-major, fp64.  See sdc_oracle.c for citations.
+ */
+#ifndef SDC_ORACLE_H
+#define SDC_ORACLE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_STOP_FIXED = 0, ORC_STOP_RTEST = 1, ORC_STOP_E21 = 2 };
+enum { ORC_STATUS_SPLIT = 0, ORC_STATUS_NO_SPLIT = 1, ORC_STATUS_NONFINITE = 2 };
+#define ORC_SPLIT_ACCEPT 1e-8 /* split_accept_tol (SPEC.md design decision; Q4) */
+
+typedef struct {
+  int k;             /* n - r: eigenvalues strictly inside the unit circle   */
+  int r;             /* order of the leading (|lambda| > 1) block            */
+  double metric;     /* ||E21||_1/||A||_1 (+ ||F21||_1/||B||_1)              */
+  double metric_fro; /* ||E21||_F/||A||_F (+ F21) at the same r              */
+  int iters;         /* IRS passes executed                                   */
+  int converged;     /* 1 if the stop rule fired before max_iters             */
+  int status;        /* ORC_STATUS_*                                          */
+} orc_result;
+
+void orc_geqr2(int m, int n, double *A, int lda, double *tau);
+void orc_apply_qt(int m, int n, const double *Y, int ldy, const double *tau,
+                  int nc, double *C, int ldc);
+void orc_org2r_signed(int n, const double *Y, int ldy, const double *tau, double *Q, int ldq);
+void orc_complement(int n, const double *Y, int ldy, const double *tau, double *C, int ldc);
+void orc_gerq2(int n, double *A, int lda, double *tau);
+void orc_orgr2_signed(int n, const double *Y, int ldy, const double *tau, double *Q, int ldq);
+void orc_geql2(int n, double *A, int lda, double *tau);
+void orc_org2l_signed(int n, const double *Y, int ldy, const double *tau, double *Q, int ldq);
+void orc_gemm(int ta, int tb, int m, int n, int K, const double *A, int lda,
+              const double *B, int ldb, double *C, int ldc);
+double orc_norm1(int m, int n, const double *X, int ldx);
+void orc_irs_pass(int n, const double *Aj, int lda, const double *Bj, int ldb,
+                  double *Aout, int ldao, double *Bout, int ldbo, double *Rout);
+void orc_grurv_right(int n, const double *Ap, int ldap, const double *Bp, int ldbp,
+                     const double *V, int ldv, double *Q, int ldq, double *R1, double *R2);
+void orc_grurv_left(int n, const double *Ap, int ldap, const double *Bp, int ldbp,
+                    const double *VL, int ldv, double *QL, int ldq);
+double orc_split_select(int n, const double *Ah, int ldah, double normA,
+                        const double *Bh, int ldbh, double normB, int *r_out, double *mvals);
+int orc_split(int n, const double *A, int lda, const double *B, int ldb,
+              const double *V, int ldv, const double *VL, int ldvl,
+              int max_iters, double tol, int stop_mode,
+              double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
+              double *hist, int hist_cap, orc_result *res);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,63 @@
+"""Mutation check for the oracle pins: apply plausible mistakes to oracle/sdc_oracle.c one at
+a time, rebuild, and confirm that the -m "not gpu" oracle tests catch each one.
+Run: python tools/oracle_mutation_check.py   (restores the original source afterwards)."""
+import os
+import shutil
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "oracle", "sdc_oracle.c")
+MUTANTS = [
+    ("swap Q12/Q22", "orc_gemm(1, 0, n, n, n, C, m, Aj, lda, Anew, n);",
+     "orc_gemm(1, 0, n, n, n, C + n, m, Aj, lda, Anew, n);"),
+    ("stack sign +A", "EL(S, n + i, j, m) = -EL(Aj, i, j, lda);", "EL(S, n + i, j, m) = EL(Aj, i, j, lda);"),
+    ("X = A_p V (not V^T)", "orc_gemm(0, 1, n, n, n, Ap, ldap, V, ldv, X, n);",
+     "orc_gemm(0, 0, n, n, n, Ap, ldap, V, ldv, X, n);"),
+    ("beta sign", "double beta = -sgn_nonneg(a) * nrm;", "double beta = sgn_nonneg(a) * nrm;"),
+    ("no R sign fix", "(i <= j) ? sgn_nonneg(EL(S, i, i, m)) * EL(S, i, j, m) : 0.0;",
+     "(i <= j) ? EL(S, i, j, m) : 0.0;"),
+    ("split row off-by-one", "sa[c] += fabs(EL(Ah, r, c, ldah));", "sa[c] += fabs(EL(Ah, r - 1, c, ldah));"),
+    ("tie -> largest r", "if (m[r] < m[best]) best = r;", "if (m[r] <= m[best]) best = r;"),
+    ("complement from [I;0]", "(i == n + j) ? 1.0 : 0.0;", "(i == j) ? 1.0 : 0.0;"),
+    ("RQ explicit Q not transposed", "EL(Q, i, j, ldq) = EL(Qrq, j, i, n);", "EL(Q, i, j, ldq) = EL(Qrq, i, j, n);"),
+    ("GRURV uses A_p - B_p", "EL(Cm, i, j, n) = EL(Ap, i, j, ldap) + EL(Bp, i, j, ldbp);",
+     "EL(Cm, i, j, n) = EL(Ap, i, j, ldap) - EL(Bp, i, j, ldbp);"),
+    ("reflector skips last row", "for (int i = k + 1; i < m; ++i) w += EL(A, i, k, lda) * EL(A, i, j, lda);",
+     "for (int i = k + 1; i < m - 1; ++i) w += EL(A, i, k, lda) * EL(A, i, j, lda);"),
+    ("QL_left uses A'_p not A'_p^T", "orc_gemm(1, 0, n, n, n, Ap, ldap, U, n, Z, n);",
+     "orc_gemm(0, 0, n, n, n, Ap, ldap, U, n, Z, n);"),
+    ("norm uses normB for A", "m[r] = ma / normA + (Bh ? mb / normB : 0.0);",
+     "m[r] = ma / normB + (Bh ? mb / normA : 0.0);"),
+]
+
+
+def main():
+    orig = open(SRC).read()
+    shutil.copy(SRC, SRC + ".orig")
+    failures = []
+    try:
+        for name, old, new in MUTANTS:
+            assert orig.count(old) == 1, f"pattern not unique/found for {name}"
+            open(SRC, "w").write(orig.replace(old, new))
+            r = subprocess.run([sys.executable, "-c", "import oracle; oracle.build(force=True)"],
+                               cwd=ROOT, capture_output=True)
+            if r.returncode:
+                print(f"{name}: build failed"); failures.append(name); continue
+            t = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "tests/test_oracle_factorizations.py",
+                                "tests/test_oracle_irs_grurv.py", "tests/test_oracle_step.py"],
+                               cwd=ROOT, capture_output=True, text=True)
+            caught = t.returncode != 0
+            print(f"{'CAUGHT ' if caught else 'MISSED '} {name}")
+            if not caught:
+                failures.append(name)
+    finally:
+        open(SRC, "w").write(orig)
+        os.remove(SRC + ".orig")
+        subprocess.run([sys.executable, "-c", "import oracle; oracle.build(force=True)"], cwd=ROOT)
+    print("missed:", failures)
+    return 1 if failures else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
