@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py -- split steps/s and effective FP64 TFLOP/s of one inverse-free split step.
+
+Workload (BASELINE.json metric "at n=16384"): configs[4] -- n = 16384 RNEP, A = U T U^T
+(seed 6), 30 IRS passes, Haar V (seed 1006); synthetic inputs resident in HBM.  One "step"
+is one full sdc_split (30 IRS passes + GRURV + similarity + split selection).  Inputs (2 GiB
+each) exceed the 126 MB L2, so no L2 flush is needed between steps.
+
+Multi-GPU: the step does not shard ("replicas only"): each rank runs its own
+independent split; value = N / (max-over-ranks time per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--n N]
+  python bench.py --impl reference ...   # the CPU oracle arm (bounded sample, extrapolated)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "split steps/s and effective FP64 TFLOP/s at n=16384 vs FP64 tensor-core peak"
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA.8x8x4 peak, profiles/r01_fp64_peak_microbench.txt
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def flop_model(n: int, passes: int, pencil: bool = False, monitor: bool = False) -> float:
+    """Paper's flop model (PAPER.md:923-945 with Lemma A1):
+    per IRS pass 40/3 n^3 (QR 10/3 + complement 6 + 2 GEMMs 4), GRURV + similarity 12 n^3;
+    monitor mode (split after every pass) 76/3 n^3 per pass; pencil doubles IRS and GRURV."""
+    n3 = float(n) ** 3
+    if monitor:
+        return passes * (76.0 / 3.0) * n3 * (2 if pencil else 1)
+    if pencil:
+        return (80.0 * passes / 3.0 + 24.0) * n3
+    return (40.0 * passes / 3.0 + 12.0) * n3
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(MEASURED))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines()]
+        except Exception:
+            rows = []
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle: a bounded sample, extrapolated by the flop model
+# ---------------------------------------------------------------------------------------
+def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 768):
+    """Time the plain oracle (as it stands) on a same-recipe sample at n_sample:
+    1 pass (+GRURV/similarity/select) and 2 passes; per-pass = difference.  Returns the
+    extrapolated seconds of one full step at n_target (n^3 scaling of each part)."""
+    import oracle
+    from paper_1011_3077_b200 import inputs
+    oracle.build()
+    threads = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    p = inputs.make_config(4 if pencil else 5, n=n_sample)
+    t = []
+    for iters in (1, 2):
+        t0 = time.perf_counter()
+        oracle.split(p.A, p.B, p.V, p.VL, max_iters=iters)
+        t.append(time.perf_counter() - t0)
+    per_pass = max(t[1] - t[0], 1e-9)
+    rest = max(t[0] - per_pass, 1e-9)
+    scale = (n_target / n_sample) ** 3
+    total = (passes * per_pass + rest) * scale
+    sample = (f"oracle.split at n={n_sample} (same recipe) with 1 and 2 passes: "
+              f"{per_pass:.2f} s/pass, {rest:.2f} s GRURV+similarity+select; extrapolated by n^3 "
+              f"to n={n_target}, {passes} passes")
+    return total, threads, sample, sum(t)
+
+
+def run_reference(args, cfg_name, n, passes, pencil, rank, world):
+    if rank != 0:
+        return 0
+    steps = []
+    threads = len(os.sched_getaffinity(0))
+    sample = ""
+    for i in range(args.warmup + args.steps):
+        total, threads, sample, _ = oracle_sample(n, passes, pencil, n_sample=args.ref_n)
+        if i >= args.warmup:
+            steps.append(total)
+    t = statistics.median(steps)
+    val = 1.0 / t
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "split steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg_name, "n": n, "passes": passes},
+            "tflops_effective": flop_model(n, passes, pencil) / t / 1e12,
+            "cpu_baseline": {"value": val, "unit": "split steps/s", "cores": threads,
+                             "kind": "oracle", "sample": sample + " (extrapolated)"},
+            "e2e": {"value": val, "unit": "split steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--n", type=int, default=None, help="override n (NOT the headline workload)")
+    ap.add_argument("--passes", type=int, default=None)
+    ap.add_argument("--impl", default="sdc", choices=["sdc", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=768)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1011_3077_b200 import inputs
+    cfg = args.config
+    n = args.n or inputs.CONFIG_N[cfg]
+    pencil = cfg == 4
+    cfg_name = f"cfg{cfg}: " + inputs.CONFIG_DOC[cfg] + ("" if args.n is None else f" [n overridden to {n}]")
+
+    if args.impl == "reference":
+        passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30}[cfg]
+        return run_reference(args, cfg_name, n, passes, pencil, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1011_3077_b200 import api
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t_in = time.perf_counter()
+    p = inputs.make_config(cfg, n=n, device=dev)
+    passes = args.passes or p.max_iters
+    stop = {0: "fixed", 1: "rtest", 2: "e21"}[p.stop]
+    torch.cuda.synchronize()
+    t_in = time.perf_counter() - t_in
+    h = api.Handle(n, pencil=pencil, device=local)
+    Q = api.empty_colmajor(n, n, dev)
+    QL = api.empty_colmajor(n, n, dev) if pencil else None
+
+    def step():
+        return h.split(p.A, p.B, p.V, p.VL, max_iters=passes, tol=p.tol, stop=stop, Q=Q, QL=QL)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = h.launches
+    h.profile(True)
+    infos = []
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(st)
+        for _ in range(args.steps):
+            _, _, _, info = step()
+            infos.append(info)
+        e1.record(st)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = (h.launches - launches0) // args.steps
+    prof = {c: h.profile_read(c) for c in range(4)}
+    h.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    info = infos[-1]
+    F = flop_model(n, info.iters, pencil, monitor=(stop == "e21"))
+    value = world / (ms / 1e3)
+    tflops = F / (ms / 1e3) / 1e12
+
+    # ---- end to end: host buffers through the C ABI, copies inside the timed region ----
+    e2e = None
+    if args.e2e_steps > 0:
+        def pinned(x):
+            if x is None:
+                return None
+            hx = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+            hx.copy_(x.t())                          # row-major (n,n) of x^T == x col-major
+            return hx.numpy().T                      # Fortran-ordered view, no copy
+        hA, hB, hV, hVL = pinned(p.A), pinned(p.B), pinned(p.V), pinned(p.VL)
+        hQ = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy().T
+        hQL = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy().T if pencil else None
+        h.split_host(hA, hB, hV, hVL, max_iters=passes, tol=p.tol, stop=stop, Q=hQ, QL=hQL)
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(st)
+        for _ in range(args.e2e_steps):
+            h.split_host(hA, hB, hV, hVL, max_iters=passes, tol=p.tol, stop=stop, Q=hQ, QL=hQL)
+        e1.record(st)
+        barrier()
+        ms_e2e = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([ms_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e2e = float(t.item())
+        nin = 2 + (2 if pencil else 0)
+        e2e = {"value": world / (ms_e2e / 1e3), "unit": "split steps/s",
+               "h2d_bytes_per_step": nin * n * n * 8, "d2h_bytes_per_step": (2 if pencil else 1) * n * n * 8,
+               "ms_per_step": ms_e2e, "steps": args.e2e_steps}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel class (DMMA GEMMs) -----------------------------
+    g_ms, g_n, g_flops = prof[0]
+    p_ms, p_n, p_bytes = prof[1]
+    hbm, hbm_src = hbm_peak()
+    achieved = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
+    roof = {"bound": "tensor", "kernel": "gemm_dmma_kernel (all DMMA GEMM launches)",
+            "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+            "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak_microbench.txt)",
+            "share_of_step": (g_ms / args.steps) / ms if ms > 0 else None,
+            "launches_per_step": g_n // max(1, args.steps),
+            "flops_per_launch": g_flops / max(1, g_n)}
+    panel = {"bound": "hbm", "kernel": "panel_qr_kernel", "achieved":
+             (p_bytes / (p_ms / 1e3) / 1e9) if p_ms > 0 else None, "peak": hbm, "unit": "GB/s",
+             "peak_source": hbm_src, "share_of_step": (p_ms / args.steps) / ms if ms > 0 else None,
+             "launches_per_step": p_n // max(1, args.steps)}
+    if panel["achieved"]:
+        panel["frac"] = panel["achieved"] / hbm
+    others = {name: {"ms_per_step": prof[c][0] / args.steps, "launches_per_step": prof[c][1] // args.steps}
+              for c, name in ((2, "k_wy_reduce"), (3, "split_select"))}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        total, threads, sample, spent = oracle_sample(n, info.iters, pencil, n_sample=args.ref_n)
+        cpu = {"value": 1.0 / total, "unit": "split steps/s", "cores": threads, "kind": "oracle",
+               "sample": sample + " (extrapolated)", "cpu_seconds_spent": spent}
+
+    clocks = clk.summary()
+    line = {"metric": METRIC, "value": value, "unit": "split steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg_name, "n": n, "passes": info.iters, "stop": stop,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs and working set (>= 2 GiB per matrix) exceed L2; no flush needed"},
+            "tflops_effective": tflops, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+            "frac_of_fp64_peak": tflops / FP64_PEAK_TFLOPS,
+            "frac_of_clock_adjusted_peak": (tflops / (FP64_PEAK_TFLOPS * clocks["sm_mhz"] / 1965.0))
+            if clocks.get("sm_mhz") else None,
+            "flop_model": F,
+            "result": {"k": info.k, "r": info.r, "metric": info.metric, "status": info.status,
+                       "expected_k": p.expected_k},
+            "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roof, "roofline_panel": panel, "other_kernels": others,
+            "cpu_baseline": cpu, "input_gen_s": t_in}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * sdc.h -- C ABI of libsdc.so: one inverse-free split step of randomized spectral
+ * divide-and-conquer (arXiv 1011.3077, Ballard-Demmel-Dumitriu) on one B200 (sm_100a).
+ *
+ * The step (PAPER.md:335-354 problem statement; Alg. 3/4/5 at PAPER.md:358-423):
+ *   1. IRS (Alg. 3): for j = 0..p-1:  [B_j; -A_j] = Q [R_j; 0],
+ *                    A_{j+1} = Q12^T A_j,  B_{j+1} = Q22^T B_j
+ *   2. Q = GRURV(2, A_p+B_p, A_p; -1, +1)  with the caller's Haar V
+ *      (and, for a pencil, Q_L = GRURV(2, A'_p^T, (A'_p+B'_p)^T; +1,-1) on IRS(A^T,B^T),
+ *       PAPER.md:387-388)
+ *   3. Ahat = Q_L^T A Q  (Q_L = Q when B = I)
+ *   4. r = argmin_{1<=r<=n-1} ||Ahat(r+1:n,1:r)||_1/||A||_1 (+ ||Bhat21||_1/||B||_1),
+ *      ties -> smallest r
+ *
+ * Polarity (reading Q1): (A_p+B_p)^{-1}A_p -> projector onto the |lambda| > 1
+ * right deflating subspace, so Q(:,1:r) spans the OUTSIDE subspace,
+ * Ahat(1:r,1:r) holds the eigenvalues with |lambda| > 1, and k = n - r is the number of
+ * eigenvalues strictly inside the unit circle (the north_star's split index).
+ *
+ * Conventions for every function below:
+ *   - matrices: IEEE fp64, column-major, element (i,j) at ptr[i + j*ld], ld >= rows;
+ *   - device pointers live on the handle's device and are caller-owned; inputs are
+ *     never modified; outputs must not alias inputs or each other;
+ *   - all GPU work is enqueued on `stream` (a cudaStream_t, NULL = legacy default);
+ *     functions returning host results synchronise that stream before returning;
+ *   - return value 0 = success; -i = argument i invalid (LAPACK style, 1-based position);
+ *     SDC_ERR_CUDA (-100) = CUDA error, SDC_ERR_NOMEM (-101) = out of memory,
+ *     SDC_ERR_NOT_SUPPORTED (-102); text of the last error via sdc_last_error();
+ *   - numerical outcomes (no split, non-finite) are NOT errors: see sdc_result.status;
+ *   - no CPU fallback: without a usable sm_100 device every call fails with -100/-102.
+ *   - a handle is not re-entrant: use one handle per concurrent stream.
+ */
+#ifndef SDC_H
+#define SDC_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDC_ERR_CUDA (-100)
+#define SDC_ERR_NOMEM (-101)
+#define SDC_ERR_NOT_SUPPORTED (-102)
+
+/* stop rules of the IRS loop */
+enum {
+  SDC_STOP_FIXED = 0, /* exactly max_iters passes                                          */
+  SDC_STOP_RTEST = 1, /* Alg. 3 line 4: stop after pass j >= 1 when
+                         ||R_j - R_{j-1}||_1 <= tol ||R_{j-1}||_1; p = j+1    */
+  SDC_STOP_E21 = 2    /* PAPER.md:597 protocol: full split after every pass, stop at the
+                         first pass whose metric <= tol (one host sync per pass)            */
+};
+enum { SDC_REGION_UNIT_DISK = 0 }; /* the only region of the step          */
+enum { SDC_STATUS_SPLIT = 0, SDC_STATUS_NO_SPLIT = 1, SDC_STATUS_NONFINITE = 2 };
+#define SDC_SPLIT_ACCEPT 1e-8 /* status 0 iff metric <= this (reading Q4)       */
+
+typedef struct {
+  int k;             /* n - r: eigenvalues strictly inside the unit circle                  */
+  int r;             /* order of the leading block (|lambda| > 1), 1 <= r <= n-1            */
+  double metric;     /* ||E21||_1/||A||_1 (+ ||F21||_1/||B||_1) at r                        */
+  double metric_fro; /* ||E21||_F/||A||_F (+ F21 term) at r (diagnostic)                    */
+  int iters;         /* IRS passes executed (p)                                            */
+  int converged;     /* 1 if the RTEST/E21 stop rule fired before max_iters                 */
+  int status;        /* SDC_STATUS_*                                                       */
+} sdc_result;
+
+typedef struct sdc_handle sdc_handle;
+
+/* Create a handle on CUDA device `device` with workspace for matrices up to n_max
+ * (pencil != 0 also reserves the RGNEP buffers).  Workspace ~ 17 n_max^2 doubles
+ * (RNEP) / 25 n_max^2 (pencil).  Supported: 2 <= n_max <= 24576.  Returns 0 or <0. */
+int sdc_create(sdc_handle** h, int device, int n_max, int pencil);
+void sdc_destroy(sdc_handle* h);
+
+/* The split step (RNEP, Alg. 5, when B == NULL; RGNEP, Alg. 4, otherwise).
+ *  1 h          handle
+ *  2 stream     cudaStream_t to enqueue on
+ *  3 n          order, 2 <= n <= n_max   (n < 2 is an error)
+ *  4 A, 5 lda   input A (device)
+ *  6 B, 7 ldb   input B (device) or NULL for B = I
+ *  8 V, 9 ldv   Haar V for Q_R (Alg. 1 lines 1-2 are done by the caller; X = A_p V^T)
+ * 10 VL,11 ldvl Haar V for Q_L; required iff B != NULL (ignored otherwise)
+ * 12 region     SDC_REGION_UNIT_DISK
+ * 13 max_iters  >= 1: number of IRS passes (cap for RTEST/E21)
+ * 14 tol        >= 0: R-test tau (RTEST) or metric threshold (E21); unused for FIXED
+ * 15 stop_mode  SDC_STOP_*
+ * 16 Q, 17 ldq  out (device): Q (= Q_R), n x n orthogonal
+ * 18 QL,19 ldql out (device): Q_L for pencils, or NULL
+ * 20 Ahat,21 ldah optional out (device): Q_L^T A Q, or NULL
+ * 22 hist, 23 hist_cap optional HOST buffer, hist_cap rows of 3 doubles per pass j:
+ *              {r*, metric} (E21 mode only, else NaN) and the R-test ratio
+ *              ||R_j - R_{j-1}||_1/||R_{j-1}||_1 of the right IRS (NaN at j = 0)
+ * 24 res       HOST out
+ * Synchronises `stream` before returning. */
+int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+              int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
+              int max_iters, double tol, int stop_mode, double* Q, int ldq, double* QL, int ldql,
+              double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
+
+/* Same step with HOST matrices (column-major, tightly packed ld = n): copies A, B, V, VL to
+ * the device, runs sdc_split, and copies Q (and QL, Ahat when non-NULL) back -- the
+ * end-to-end path of the public API.  Host buffers may be pageable or pinned. */
+int sdc_split_host(sdc_handle* h, void* stream, int n, const double* A, const double* B,
+                   const double* V, const double* VL, int max_iters, double tol, int stop_mode,
+                   double* Q, double* QL, double* Ahat, double* hist, int hist_cap,
+                   sdc_result* res);
+
+/* ---- building blocks of the step, exported for kernel-level parity tests ---------- */
+
+/* C = alpha op(A) op(B) + beta C on the FP64 tensor cores (DMMA); op = transpose when
+ * transa/transb != 0.  M x N result, K inner.  PAPER.md:916 (matrix multiply). */
+int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N, int K,
+              double alpha, const double* A, int lda, const double* B, int ldb, double beta,
+              double* C, int ldc);
+
+/* Blocked Householder QR of the m x n matrix A (m >= n, m <= 2 n_max, n <= n_max) in
+ * place: on return R (with the LAPACK-sign diagonal) is in the upper triangle.
+ * If Qthin != NULL it receives the explicit m x n Q with diag(R) made >= 0 (the rows
+ * of R are NOT sign-fixed in A; use the signs of diag(A) to do so).  PAPER.md:331. */
+int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double* Qthin,
+           int ldq);
+
+/* One IRS pass (Alg. 3 line 3): Aout = Q12^T A, Bout = Q22^T B for [B; -A] = Q [R; 0],
+ * and Rout (n x n, optional) = R with non-negative diagonal. */
+int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+                 int ldb, double* Aout, int ldao, double* Bout, int ldbo, double* Rout, int ldr);
+
+/* Split selection on Ahat (and Bhat, or NULL) with the given norms:
+ * returns r (1..n-1, ties -> smallest) and the metric on the host; mvals (optional,
+ * DEVICE, length n) receives m(r) at index r (index 0 unused). */
+int sdc_split_select(sdc_handle* h, void* stream, int n, const double* Ahat, int ldah,
+                     double normA, const double* Bhat, int ldbh, double normB, int* r,
+                     double* metric, double* mvals);
+
+/* Per-kernel-class timing with CUDA events recorded on the launching stream around every
+ * launch of the class (measurement support for bench.py's roofline numbers).
+ * sdc_profile(h, 1) resets the counters and starts recording, (h, 0) stops.
+ * sdc_profile_read returns, for class cls, the summed event time (ms), the number of
+ * launches and the summed ALGORITHMIC work: flops 2MNK for SDC_PROF_GEMM, bytes
+ * (read + write of the operands the definition touches) for the other classes. */
+enum { SDC_PROF_GEMM = 0, SDC_PROF_PANEL = 1, SDC_PROF_WYRED = 2, SDC_PROF_SELECT = 3,
+       SDC_PROF_CLASSES = 4 };
+int sdc_profile(sdc_handle* h, int enable);
+int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, double* work);
+
+/* Number of kernels launched by this handle since creation (evidence counter). */
+long long sdc_kernel_launches(const sdc_handle* h);
+
+/* Text of the last error on this thread ("" if none). */
+const char* sdc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDC_H */

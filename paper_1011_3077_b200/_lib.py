@@ -1,0 +1,68 @@
+"""ctypes declarations of libsdc.so (include/sdc.h).  Argument marshalling only."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsdc.so")
+
+STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
+STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
+REGION_UNIT_DISK = 0
+PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT = 0, 1, 2, 3
+SPLIT_ACCEPT = 1e-8
+
+
+class SdcResult(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int), ("r", ctypes.c_int), ("metric", ctypes.c_double),
+                ("metric_fro", ctypes.c_double), ("iters", ctypes.c_int),
+                ("converged", ctypes.c_int), ("status", ctypes.c_int)]
+
+
+_lib = None
+P, I, D, LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
+
+_SIGS = {
+    "sdc_create": (I, [ctypes.POINTER(P), I, I, I]),
+    "sdc_destroy": (None, [P]),
+    "sdc_split": (I, [P, P, I, P, I, P, I, P, I, P, I, I, I, D, I, P, I, P, I, P, I, P, I,
+                      ctypes.POINTER(SdcResult)]),
+    "sdc_split_host": (I, [P, P, I, P, P, P, P, I, D, I, P, P, P, P, I, ctypes.POINTER(SdcResult)]),
+    "sdc_dgemm": (I, [P, P, I, I, I, I, I, D, P, I, P, I, D, P, I]),
+    "sdc_qr": (I, [P, P, I, I, P, I, P, I]),
+    "sdc_irs_pass": (I, [P, P, I, P, I, P, I, P, I, P, I, P, I]),
+    "sdc_split_select": (I, [P, P, I, P, I, D, P, I, D, ctypes.POINTER(I), ctypes.POINTER(D), P]),
+    "sdc_kernel_launches": (LL, [P]),
+    "sdc_profile": (I, [P, I]),
+    "sdc_profile_read": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(LL), ctypes.POINTER(D)]),
+    "sdc_last_error": (ctypes.c_char_p, []),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def load(path: str = LIB_PATH):
+    """Load libsdc.so.  There is no fallback: a missing library is an error."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -m paper_1011_3077_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+class SdcError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str):
+    if rc != 0:
+        msg = load().sdc_last_error().decode(errors="replace")
+        raise SdcError(f"{what} failed with {rc}: {msg}")

@@ -1,0 +1,376 @@
+// aux.cuh -- HBM-bound O(n^2) kernels of the split step: stack/identity set-up, sums,
+// index-remapped copies (transpose / reversal for RQ and QL via QR), norms, the R-test
+// (Alg. 3 line 4) and the split selection (Alg. 4 line 5 / Alg. 5 line 3).
+// All column-major; one thread per element with coalesced row-fastest indexing unless
+// noted.  Reductions use fixed orders (no atomics) so results are run-to-run identical.
+#pragma once
+#include "common.cuh"
+
+namespace sdc {
+
+// grid-stride 2-D loop over an m x n column-major index space
+#define SDC_FOR_MN(m, n)                                                                   \
+  for (long long _e = (long long)blockIdx.x * blockDim.x + threadIdx.x,                      \
+                 _tot = (long long)(m) * (n);                                              \
+       _e < _tot; _e += (long long)gridDim.x * blockDim.x)
+
+// out = alpha * identity (m x n)
+__global__ void k_set_identity(double* out, long long ld, int m, int n, double alpha) {
+  SDC_FOR_MN(m, n) {
+    int i = (int)(_e % m), j = (int)(_e / m);
+    out[i + (long long)j * ld] = (i == j) ? alpha : 0.0;
+  }
+}
+
+// out (2n x n) = [0; I]   -- initial value for the IRS complement
+__global__ void k_set_zero_identity(double* out, long long ld, int n) {
+  SDC_FOR_MN(2 * n, n) {
+    int i = (int)(_e % (2 * n)), j = (int)(_e / (2 * n));
+    out[i + (long long)j * ld] = (i == n + j) ? 1.0 : 0.0;
+  }
+}
+
+// out = op(src): trans=0 copy, trans=1 transpose (m x n result)
+__global__ void k_copy(double* out, long long ldo, const double* src, long long lds, int m, int n,
+                       double alpha) {
+  SDC_FOR_MN(m, n) {
+    int i = (int)(_e % m), j = (int)(_e / m);
+    out[i + (long long)j * ldo] = alpha * src[i + (long long)j * lds];
+  }
+}
+
+// tiled transpose-with-remap:  out(i, j) = s(j) * src(ri(i, j), rj(i, j)) where the mode
+// selects the remap (used for RQ = reversed QR of C^T J and QL = reversed QR of J X J):
+//   mode 0: out(i,j) = src(j, i)                      (transpose)
+//   mode 1: out(i,j) = src(n-1-j, i)                  (C^T J)
+//   mode 2: out(i,j) = src(n-1-i, n-1-j)              (J X J, no transpose)
+//   mode 3: out(i,j) = src(n-1-i, j)                  (J X, row reversal)
+__global__ void k_transpose_rev(double* out, long long ldo, const double* src, long long lds, int n,
+                                int mode) {
+  __shared__ double tile[32][33];
+  int bi = blockIdx.x * 32, bj = blockIdx.y * 32;
+  int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  if (mode >= 2) {
+    for (int r = ty; r < 32; r += 8) {
+      int i = bi + tx, j = bj + r;
+      int sj = mode == 2 ? n - 1 - j : j;
+      if (i < n && j < n) out[i + (long long)j * ldo] = src[(n - 1 - i) + (long long)sj * lds];
+    }
+    return;
+  }
+  // read src block (rows bj.., cols bi..) coalesced, write transposed
+  for (int r = ty; r < 32; r += 8) {
+    int sr = bj + tx, sc = bi + r;           // src row (maps to out col), src col (out row)
+    if (sr < n && sc < n) {
+      int srow = (mode == 1) ? (n - 1 - sr) : sr;
+      tile[r][tx] = src[srow + (long long)sc * lds];
+    }
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    int i = bi + tx, j = bj + r;             // out(i,j) = src(map(j), i)
+    if (i < n && j < n) out[i + (long long)j * ldo] = tile[tx][r];
+  }
+}
+
+// out = a + b (m x n)
+__global__ void k_add(double* out, long long ldo, const double* a, long long lda, const double* b,
+                      long long ldb, int m, int n) {
+  SDC_FOR_MN(m, n) {
+    int i = (int)(_e % m), j = (int)(_e / m);
+    out[i + (long long)j * ldo] = a[i + (long long)j * lda] + b[i + (long long)j * ldb];
+  }
+}
+
+// stack S (2n x n, ld lds) = [B; -A]
+__global__ void k_build_stack(double* S, long long lds, const double* A, long long lda,
+                              const double* B, long long ldb, int n) {
+  SDC_FOR_MN(2 * n, n) {
+    int i = (int)(_e % (2 * n)), j = (int)(_e / (2 * n));
+    S[i + (long long)j * lds] = (i < n) ? B[i + (long long)j * ldb] : -A[(i - n) + (long long)j * lda];
+  }
+}
+
+// rows i of X scaled by sign(diag(Rf)(i)) (sign(0)=+1): U <- U D_U applied as U^T C rows
+__global__ void k_row_sign(double* X, long long ldx, const double* Rf, long long ldr, int n, int ncols) {
+  SDC_FOR_MN(n, ncols) {
+    int i = (int)(_e % n), j = (int)(_e / n);
+    if (Rf[i + (long long)i * ldr] < 0.0) X[i + (long long)j * ldx] = -X[i + (long long)j * ldx];
+  }
+}
+
+// Q(:, j) = sign(R(jj,jj)) * Qs(:, jj) with jj = rev ? n-1-j : j   (sign fix + reversal)
+__global__ void k_col_sign_rev(double* Q, long long ldq, const double* Qs, long long lds,
+                               const double* Rf, long long ldr, int n, int rev) {
+  SDC_FOR_MN(n, n) {
+    int i = (int)(_e % n), j = (int)(_e / n);
+    int jj = rev ? n - 1 - j : j;
+    double d = Rf[jj + (long long)jj * ldr] < 0.0 ? -1.0 : 1.0;
+    Q[i + (long long)j * ldq] = d * Qs[i + (long long)jj * lds];
+  }
+}
+
+// X(:, j) *= sign(Rf(j,j))  (m x n)
+__global__ void k_col_sign(double* X, long long ldx, int m, int n, const double* Rf, long long ldr) {
+  SDC_FOR_MN(m, n) {
+    int i = (int)(_e % m), j = (int)(_e / m);
+    if (Rf[j + (long long)j * ldr] < 0.0) X[i + (long long)j * ldx] = -X[i + (long long)j * ldx];
+  }
+}
+
+// ---- norms: one warp per column -> per-column abs-sum and sum of squares ------------
+__global__ void k_colnorms(const double* X, long long ldx, int m, int n, double* colabs,
+                           double* colsq) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int j = warp; j < n; j += nw) {
+    double sa = 0.0, sq = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      double v = X[i + (long long)j * ldx];
+      sa += fabs(v);
+      sq = fma(v, v, sq);
+    }
+    sa = warp_sum(sa);
+    sq = warp_sum(sq);
+    if (lane == 0) { colabs[j] = sa; colsq[j] = sq; }
+  }
+}
+
+// single-CTA fixed-order reduction: out[0] = max_j colabs[j], out[1] = sqrt(sum_j colsq[j])
+__global__ void k_norm_finish(const double* colabs, const double* colsq, int n, double* out) {
+  __shared__ double smx[32], ssq[32];
+  double mx = 0.0, sq = 0.0;
+  bool nan = false;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double a = colabs[j];
+    nan |= (a != a);
+    mx = fmax(mx, a);
+    sq += colsq[j];
+  }
+  mx = warp_max(mx);
+  sq = warp_sum(sq);
+  nan = __any_sync(0xffffffffu, nan);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __shared__ int snan;
+  if (threadIdx.x == 0) snan = 0;
+  __syncthreads();
+  if (nan && l == 0) snan = 1;
+  if (l == 0) { smx[w] = mx; ssq[w] = sq; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double M = 0.0, Q = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { M = fmax(M, smx[i]); Q += ssq[i]; }
+    out[0] = snan ? __longlong_as_double(0x7ff8000000000000ll) : M;
+    out[1] = sqrt(Q);
+  }
+}
+
+// ---- R-test (Alg. 3 line 4) -------------------------------------------
+// R_j = D S(0:n,0:n) upper (D = sign(diag)), per column c:
+//   dabs[c] = sum_{i<=c} |R_j(i,c) - Rprev(i,c)|,  pabs[c] = sum_{i<=c} |Rprev(i,c)|
+// then Rprev <- R_j.  One warp per column.
+__global__ void k_rtest_cols(const double* S, long long lds, double* Rprev, int n, double* dabs,
+                             double* pabs) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = warp; c < n; c += nw) {
+    double sd = 0.0, sp = 0.0;
+    for (int i = lane; i <= c; i += 32) {
+      double d = S[i + (long long)i * lds] < 0.0 ? -1.0 : 1.0;
+      double r = d * S[i + (long long)c * lds];
+      double p = Rprev[i + (long long)c * n];
+      sd += fabs(r - p);
+      sp += fabs(p);
+      Rprev[i + (long long)c * n] = r;
+    }
+    sd = warp_sum(sd);
+    sp = warp_sum(sp);
+    if (lane == 0) { dabs[c] = sd; pabs[c] = sp; }
+  }
+}
+
+// ratio = max(dabs)/max(pabs) -> hist[slot] (single CTA)
+__global__ void k_rtest_finish(const double* dabs, const double* pabs, int n, double* out) {
+  __shared__ double sd[32], sp[32];
+  double md = 0.0, mp = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) { md = fmax(md, dabs[j]); mp = fmax(mp, pabs[j]); }
+  md = warp_max(md);
+  mp = warp_max(mp);
+  if ((threadIdx.x & 31) == 0) { sd[threadIdx.x >> 5] = md; sp[threadIdx.x >> 5] = mp; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double D = 0.0, P = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { D = fmax(D, sd[i]); P = fmax(P, sp[i]); }
+    *out = D / P;
+  }
+}
+
+// ---- split selection (blocked column prefix-sum, then row max) ----------
+// Stage 1: CTA b owns columns [32b, 32b+32).  Walking rows bottom-up in 32-row chunks it
+// keeps the column suffix sums s_c(r) = sum_{i >= r} |Ah(i,c)| (0-based; E21 for a leading
+// block of order r is rows r..n-1, columns 0..r-1) and writes, for every row r, the block's
+// max over its columns c < r:   pm[b][r] = max_{c in block, c < r} s_c(r).
+constexpr int SEL_T = 32;
+__global__ void __launch_bounds__(256) k_select_cols(const double* Ah, long long lda, int n,
+                                                     double* pm) {
+  __shared__ double tile[SEL_T][SEL_T + 1];   // [row][col]
+  const int b = blockIdx.x, c0 = b * SEL_T;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  double run = 0.0;                            // running suffix sum of column c0+tx (warp 0)
+  const int nchunks = (n + SEL_T - 1) / SEL_T;
+  for (int ch = nchunks - 1; ch >= 0; --ch) {
+    const int rb = ch * SEL_T;
+    if (rb + SEL_T <= c0) {                    // rows all above the block's columns: only r <= c
+      // rows r < c0+1 can still need pm for r > c for some c in block: r > c >= c0 impossible
+      for (int r = threadIdx.x; r < SEL_T; r += blockDim.x)
+        if (rb + r < n) pm[(long long)b * n + rb + r] = 0.0;
+      continue;
+    }
+    for (int r = ty; r < SEL_T; r += 8) {      // coalesced: lanes along rows of one column
+      int gr = rb + tx, gc = c0 + r;
+      tile[tx][r] = (gr < n && gc < n) ? fabs(Ah[gr + (long long)gc * lda]) : 0.0;
+    }
+    __syncthreads();
+    if (ty == 0) {
+      // lane tx = column c0+tx: suffix sums bottom-up within the chunk (row order n-1 -> 0)
+      for (int r = SEL_T - 1; r >= 0; --r) {
+        run += tile[r][tx];
+        tile[r][tx] = run;                     // s_c(rb + r)
+      }
+    }
+    __syncthreads();
+    if (ty == 0) {
+      // lane tx = row rb+tx: max over block columns c < row
+      int gr = rb + tx;
+      double mx = 0.0;
+      for (int c = 0; c < SEL_T; ++c)
+        if (c0 + c < gr && c0 + c < n) mx = fmax(mx, tile[tx][c]);
+      if (gr < n) pm[(long long)b * n + gr] = mx;
+    }
+    __syncthreads();
+  }
+}
+
+// Stage 2: m(r) = max_{b} pm[b][r] / normA (+ same for B), r = 1..n-1 -> mvals[r]
+__global__ void k_select_rows(const double* pmA, const double* pmB, int n, int nblk,
+                              const double* normA, const double* normB, double* mvals) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < 1 || r >= n) return;
+  int bmax = min(nblk, (r + SEL_T - 1) / SEL_T);   // blocks with c0 < r
+  double ma = 0.0, mb = 0.0;
+  for (int b = 0; b < bmax; ++b) {
+    ma = fmax(ma, pmA[(long long)b * n + r]);
+    if (pmB) mb = fmax(mb, pmB[(long long)b * n + r]);
+  }
+  mvals[r] = ma / normA[0] + (pmB ? mb / normB[0] : 0.0);
+}
+
+// Stage 3 (single CTA, 1024 threads): argmin over r = 1..n-1, ties -> smallest r
+// (SPEC.md:255); out = {r, metric}.  NaN never wins a comparison; all-NaN -> r = 1.
+__global__ void __launch_bounds__(1024) k_select_argmin(const double* mvals, int n, double* out) {
+  __shared__ double sv[1024];
+  __shared__ int si[1024];
+  const int NONE = 0x7fffffff;
+  double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  int bi = NONE;
+  for (int r = 1 + threadIdx.x; r < n; r += blockDim.x) {
+    double v = mvals[r];
+    if (v < best) { best = v; bi = r; }
+  }
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = blockDim.x >> 1; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      double v2 = sv[threadIdx.x + s];
+      int i2 = si[threadIdx.x + s];
+      if (v2 < sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int r = si[0] == NONE ? 1 : si[0];
+    out[0] = (double)r;
+    out[1] = mvals[r];
+  }
+}
+
+// ||Ah(r:n, 0:r)||_F^2 per column (warp per column), r read from sel[0]
+__global__ void k_e21_fro_cols(const double* Ah, long long lda, int n, const double* sel,
+                               double* colsq) {
+  int r = (int)sel[0];
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = warp; c < n; c += nw) {
+    double s = 0.0;
+    if (c < r)
+      for (int i = r + lane; i < n; i += 32) { double v = Ah[i + (long long)c * lda]; s = fma(v, v, s); }
+    s = warp_sum(s);
+    if (lane == 0) colsq[c] = s;
+  }
+}
+
+// out = sqrt(sum colsqA)/froA (+ sqrt(sum colsqB)/froB), single CTA, fixed order
+__global__ void k_e21_fro_finish(const double* colsqA, const double* colsqB, int n,
+                                 const double* nrmA, const double* nrmB, double* out) {
+  __shared__ double sa[32], sb[32];
+  double a = 0.0, b = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) { a += colsqA[j]; if (colsqB) b += colsqB[j]; }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if ((threadIdx.x & 31) == 0) { sa[threadIdx.x >> 5] = a; sb[threadIdx.x >> 5] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double A = 0.0, B = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { A += sa[i]; B += sb[i]; }
+    *out = sqrt(A) / nrmA[1] + (colsqB ? sqrt(B) / nrmB[1] : 0.0);
+  }
+}
+
+// non-finite scan: flag[0] |= any(!isfinite(X))
+__global__ void k_nonfinite(const double* X, long long ldx, int n, int* flag) {
+  bool bad = false;
+  SDC_FOR_MN(n, n) {
+    int i = (int)(_e % n), j = (int)(_e / n);
+    double v = X[i + (long long)j * ldx];
+    bad |= !isfinite(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+// WY reduction for split-K partials:  W(:, c) = op(T) * sum_s Wp[s](:, c)
+//   trans = 1: W = T^T W0 (apply H^T = I - Y T^T Y^T, i.e. Q^T C);  trans = 0: W = T W0.
+// One CTA (256 threads) per block of WYR_COLS columns; T staged in smem.
+constexpr int WYR_COLS = 16;
+__global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits, long long zstride,
+                                                   int nb, int ncols, const double* T, int trans,
+                                                   double* W) {
+  __shared__ double Ts[64 * 64];
+  __shared__ double w0[WYR_COLS][64];
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) Ts[e] = T[e];
+  const int c0 = blockIdx.x * WYR_COLS;
+  for (int e = threadIdx.x; e < WYR_COLS * nb; e += blockDim.x) {
+    int cc = e / nb, i = e % nb, c = c0 + cc;
+    double s = 0.0;
+    if (c < ncols)
+      for (int z = 0; z < splits; ++z) s += Wp[(long long)z * zstride + i + (long long)c * nb];
+    w0[cc][i] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < WYR_COLS * nb; e += blockDim.x) {
+    int cc = e / nb, i = e % nb, c = c0 + cc;
+    if (c >= ncols) continue;
+    double s = 0.0;
+    if (trans) {   // (T^T w)(i) = sum_{l <= i} T(l, i) w(l)
+      for (int l = 0; l <= i; ++l) s = fma(Ts[i * nb + l], w0[cc][l], s);
+    } else {       // (T w)(i) = sum_{l >= i} T(i, l) w(l)
+      for (int l = i; l < nb; ++l) s = fma(Ts[l * nb + i], w0[cc][l], s);
+    }
+    W[i + (long long)c * nb] = s;
+  }
+}
+
+}  // namespace sdc

@@ -1,0 +1,792 @@
+// sdc.cu -- libsdc.so: host orchestration + C ABI (include/sdc.h) of one inverse-free
+// split step on one B200 (sm_100a).  Every arithmetic step runs in the kernels of
+// gemm.cuh (FP64 tensor-core DMMA), panel.cuh (Householder panels) and aux.cuh (O(n^2)
+// passes); this file only sequences them on the caller's stream and owns the workspace.
+//
+// Step structure:
+//   IRS pass j (Alg. 3):  blocked Householder QR of S = [B_j; -A_j] (panels + WY
+//     trailing updates), complement [Q12;Q22] = H_0..H_{n-1}[0;I] (backward WY), then
+//     A_{j+1} = Q12^T A_j, B_{j+1} = Q22^T B_j whose epilogue also writes the next stack.
+//   GRURV (Alg. 1/2):  X = A_p V^T, QR(X) -> U, C = U^T (A_p+B_p), RQ(C) computed as the
+//     QR of C^T J with explicit Q, Q = Q_qr D J (reading Q10).
+//   Similarity Q_L^T A Q and split selection.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/sdc.h"
+#include "aux.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "panel.cuh"
+
+using namespace sdc;
+
+namespace {
+
+thread_local char g_err[1024] = "";
+
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define SDC_CK(x)                                                              \
+  do {                                                                         \
+    cudaError_t e_ = (x);                                                      \
+    if (e_ != cudaSuccess) {                                                   \
+      set_err("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      return e_ == cudaErrorMemoryAllocation ? SDC_ERR_NOMEM : SDC_ERR_CUDA;  \
+    }                                                                          \
+  } while (0)
+#define SDC_TRY(x)            \
+  do {                        \
+    int rc_ = (x);            \
+    if (rc_ != 0) return rc_; \
+  } while (0)
+
+constexpr int NB = PANEL_NB;       // panel / WY block width
+constexpr int SCAL_HIST = 8;       // scal[8 + j]: R-test ratio of pass j
+constexpr int MAX_HIST = 65536;
+
+}  // namespace
+
+struct sdc_handle {
+  int device = 0, n_max = 0, pencil = 0, num_sms = 0;
+  cudaStream_t st = nullptr;
+  // workspace (see sdc_create for sizes)
+  double *S = nullptr, *SL = nullptr, *Y = nullptr, *C = nullptr;
+  double *A[2] = {nullptr, nullptr}, *B[2] = {nullptr, nullptr};
+  double *AL[2] = {nullptr, nullptr}, *BL[2] = {nullptr, nullptr};
+  double *G1 = nullptr, *G2 = nullptr, *G3 = nullptr, *T1 = nullptr, *Ah = nullptr, *Bh = nullptr;
+  double *QLb = nullptr, *Rprev = nullptr;
+  double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
+  double *pmA = nullptr, *pmB = nullptr, *vec = nullptr, *scal = nullptr;
+  size_t wp_elems = 0;
+  unsigned int* bar = nullptr;
+  unsigned long long bar_count = 0;
+  int* flag = nullptr;
+  long long launches = 0;
+  // optional per-kernel-class timing with CUDA events on the launching stream
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct ProfRec { int cls; int e0, e1; double work; };
+  std::vector<ProfRec> recs;
+  double prof_ms[SDC_PROF_CLASSES] = {0}, prof_work[SDC_PROF_CLASSES] = {0};
+  long long prof_n[SDC_PROF_CLASSES] = {0};
+  // staging for sdc_split_host
+  double *hA = nullptr, *hB = nullptr, *hV = nullptr, *hVL = nullptr, *hQ = nullptr,
+         *hQL = nullptr, *hAh = nullptr;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int dalloc(sdc_handle* h, double** p, size_t elems) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(elems, 1) * sizeof(double));
+  if (e != cudaSuccess) {
+    set_err("cudaMalloc(%zu doubles): %s", elems, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? SDC_ERR_NOMEM : SDC_ERR_CUDA;
+  }
+  h->allocs.push_back(q);
+  *p = static_cast<double*>(q);
+  return 0;
+}
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+inline bool al16(const void* p, long long ld) {
+  return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (ld % 2 == 0);
+}
+inline int ew_grid(long long elems) { return (int)std::min<long long>(cdiv(elems, 256), 148LL * 16); }
+
+#define SDC_LAUNCHED(h)                                                            \
+  do {                                                                             \
+    (h)->launches++;                                                               \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess) {                                                       \
+      set_err("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(e_));     \
+      return SDC_ERR_CUDA;                                                         \
+    }                                                                              \
+  } while (0)
+
+// ---- per-class CUDA-event timing (sdc_profile) --------------------------------------
+int prof_event(sdc_handle* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    h->ev_pool.push_back(e);
+  }
+  int id = (int)h->ev_used++;
+  cudaEventRecord(h->ev_pool[id], h->st);
+  return id;
+}
+struct ProfScope {
+  sdc_handle* h; int cls; double work; int e0;
+  ProfScope(sdc_handle* h_, int cls_, double work_) : h(h_), cls(cls_), work(work_), e0(-1) {
+    if (h->prof_on) e0 = prof_event(h);
+  }
+  ~ProfScope() {
+    if (h->prof_on && e0 >= 0) {
+      int e1 = prof_event(h);
+      if (e1 >= 0) h->recs.push_back({cls, e0, e1, work});
+    }
+  }
+};
+void prof_collect(sdc_handle* h) {
+  if (h->recs.empty()) return;
+  cudaEventSynchronize(h->ev_pool[h->recs.back().e1]);
+  for (auto& r : h->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev_pool[r.e0], h->ev_pool[r.e1]);
+    h->prof_ms[r.cls] += ms;
+    h->prof_work[r.cls] += r.work;
+    h->prof_n[r.cls] += 1;
+  }
+  h->recs.clear();
+  h->ev_used = 0;
+}
+
+// ---------------------------------------------------------------------------------------
+// GEMM dispatch
+// ---------------------------------------------------------------------------------------
+using TileL = GemmTile<128, 128, 16, 64, 32, 4>;  // 8 warps, warp tile 64x32
+using TileM = GemmTile<64, 128, 16, 32, 32, 4>;   // 8 warps (W0 = Y^T C, M = nb)
+using TileS = GemmTile<64, 64, 16, 32, 32, 4>;    // 4 warps (small problems)
+
+template <class T, bool TA, bool TB, int VEC>
+int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
+  using Sm = GemmSmem<T, TA, TB>;
+  static int attr_set = 0;   // per instantiation (single device per process in practice)
+  if (!attr_set) {
+    SDC_CK(cudaFuncSetAttribute(gemm_dmma_kernel<T, TA, TB, VEC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::BYTES));
+    attr_set = 1;
+  }
+  dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
+  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K);
+  gemm_dmma_kernel<T, TA, TB, VEC><<<grid, T::THREADS, Sm::BYTES, h->st>>>(g);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+template <class T, bool TA, bool TB>
+int launch_gemm_v(sdc_handle* h, const GemmArgs& g, int splits) {
+  if (al16(g.A, g.lda) && al16(g.B, g.ldb)) return launch_gemm_t<T, TA, TB, 2>(h, g, splits);
+  return launch_gemm_t<T, TA, TB, 1>(h, g, splits);
+}
+
+template <bool TA, bool TB>
+int launch_gemm_tile(sdc_handle* h, const GemmArgs& g, int splits) {
+  if (g.M <= 64) return launch_gemm_v<TileM, TA, TB>(h, g, splits);
+  long long tilesL = (long long)cdiv(g.M, 128) * cdiv(g.N, 128) * splits;
+  if (tilesL >= h->num_sms) return launch_gemm_v<TileL, TA, TB>(h, g, splits);
+  return launch_gemm_v<TileS, TA, TB>(h, g, splits);
+}
+
+// C = alpha op(A) op(B) + beta C  [+ D2 = alpha2 op(A) op(B)]
+int gemm(sdc_handle* h, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
+         long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
+         double* D2 = nullptr, long long ldd2 = 0, double alpha2 = 0.0) {
+  if (M <= 0 || N <= 0) return 0;
+  GemmArgs g{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, D2, ldd2, alpha2, std::max(K, 1), 0};
+  if (!ta && !tb) return launch_gemm_tile<false, false>(h, g, 1);
+  if (ta && !tb) return launch_gemm_tile<true, false>(h, g, 1);
+  if (!ta && tb) return launch_gemm_tile<false, true>(h, g, 1);
+  return launch_gemm_tile<true, true>(h, g, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// compact-WY application:  C (m x ncols) <- (I - Y op(T) Y^T) C,
+//   trans = 1: op(T) = T^T  (H_{nb-1}..H_0 C, i.e. Q^T C)
+//   trans = 0: op(T) = T    (H_0..H_{nb-1} C, i.e. Q C)
+// W0 = Y^T C (split-K DMMA GEMM) -> W = op(T) W0 (k_wy_reduce) -> C -= Y W (DMMA GEMM)
+// ---------------------------------------------------------------------------------------
+int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long long ldy,
+             const double* T, int nb, double* C, long long ldc) {
+  if (m <= 0 || ncols <= 0) return 0;
+  const int tilesN = cdiv(ncols, TileM::BN);
+  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesN), std::max(1, m / 256)));
+  int kchunk = cdiv(cdiv(m, splits), 16) * 16;
+  splits = cdiv(m, kchunk);
+  if ((size_t)splits * nb * ncols > h->wp_elems) {
+    set_err("wy_apply: split-K workspace too small");
+    return SDC_ERR_CUDA;
+  }
+  GemmArgs g{nb, ncols, m, Y, ldy, C, ldc, h->Wp, nb, 1.0, 0.0, nullptr, 0, 0.0, kchunk,
+             (long long)nb * ncols};
+  SDC_TRY((launch_gemm_tile<true, false>(h, g, splits)));
+  {
+    ProfScope ps(h, SDC_PROF_WYRED, 8.0 * ((double)splits * nb * ncols + (double)nb * ncols));
+    k_wy_reduce<<<cdiv(ncols, WYR_COLS), 256, 0, h->st>>>(h->Wp, splits, (long long)nb * ncols, nb,
+                                                          ncols, T, trans, h->W);
+    SDC_LAUNCHED(h);
+  }
+  return gemm(h, false, false, m, ncols, nb, -1.0, Y, ldy, h->W, nb, 1.0, C, ldc);
+}
+
+// ---------------------------------------------------------------------------------------
+// panel (cooperative) and blocked QR
+// ---------------------------------------------------------------------------------------
+int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
+          double* T, double* tau) {
+  int G = std::min(h->num_sms, std::max(1, m / 128));
+  int rows_per = cdiv(m, G);
+  if (rows_per < nb) {
+    rows_per = nb;
+    G = cdiv(m, rows_per);
+  }
+  size_t smem = panel_smem_bytes(rows_per);
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    cudaError_t e = cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) {
+      set_err("panel: %d rows per CTA need %zu B of shared memory (n too large): %s", rows_per,
+              smem, cudaGetErrorString(e));
+      return SDC_ERR_NOT_SUPPORTED;
+    }
+    attr_smem = smem;
+  }
+  PanelArgs a{P, ldp, m, nb, Y, ldy, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count, rows_per};
+  void* args[] = {&a};
+  ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 3.0 * m * nb);   // read panel, write panel + Y
+  SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(G), dim3(PANEL_THREADS),
+                                     args, smem, h->st));
+  h->launches++;
+  h->bar_count += (unsigned long long)G * nb;
+  return 0;
+}
+
+inline double* Tblk(sdc_handle* h, int i0) { return h->Tb + (size_t)(i0 / NB) * NB * NB; }
+
+// A (m x n, m >= n) <- Householder QR in place; Y (m x n, explicit) and T blocks out.
+int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, double* Y, long long ldy) {
+  for (int i0 = 0; i0 < n; i0 += NB) {
+    int nbp = std::min(NB, n - i0);
+    double* Yp = Y + i0 + (long long)i0 * ldy;
+    SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, Yp, ldy, Tblk(h, i0),
+                  h->tau + i0));
+    if (i0 + nbp < n)
+      SDC_TRY(wy_apply(h, 1, m - i0, n - i0 - nbp, Yp, ldy, Tblk(h, i0), nbp,
+                       A + i0 + (long long)(i0 + nbp) * lda, lda));
+  }
+  return 0;
+}
+
+// C (m x ncols) <- Q^T C  (forward over panels) for the last blocked_qr of an m x n matrix
+int apply_qt(sdc_handle* h, int m, int n, const double* Y, long long ldy, double* C, long long ldc,
+             int ncols) {
+  for (int i0 = 0; i0 < n; i0 += NB) {
+    int nbp = std::min(NB, n - i0);
+    SDC_TRY(wy_apply(h, 1, m - i0, ncols, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+                     C + i0, ldc));
+  }
+  return 0;
+}
+
+// C (m x ncols) <- Q C  (backward over panels)
+int apply_q(sdc_handle* h, int m, int n, const double* Y, long long ldy, double* C, long long ldc,
+            int ncols) {
+  int last = ((n - 1) / NB) * NB;
+  for (int i0 = last; i0 >= 0; i0 -= NB) {
+    int nbp = std::min(NB, n - i0);
+    SDC_TRY(wy_apply(h, 0, m - i0, ncols, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+                     C + i0, ldc));
+  }
+  return 0;
+}
+
+// explicit square Q (n x n) = H_0..H_{n-1} (dorgqr order: only the trailing block changes)
+int form_q(sdc_handle* h, int n, const double* Y, long long ldy, double* Q, long long ldq) {
+  k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Q, ldq, n, n, 1.0);
+  SDC_LAUNCHED(h);
+  int last = ((n - 1) / NB) * NB;
+  for (int i0 = last; i0 >= 0; i0 -= NB) {
+    int nbp = std::min(NB, n - i0);
+    SDC_TRY(wy_apply(h, 0, n - i0, n - i0, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+                     Q + i0 + (long long)i0 * ldq, ldq));
+  }
+  return 0;
+}
+
+int transpose_rev(sdc_handle* h, double* out, long long ldo, const double* src, long long lds,
+                  int n, int mode) {
+  dim3 grid(cdiv(n, 32), cdiv(n, 32));
+  k_transpose_rev<<<grid, dim3(32, 8), 0, h->st>>>(out, ldo, src, lds, n, mode);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+int norms(sdc_handle* h, const double* X, long long ldx, int n, double* out2) {
+  k_colnorms<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(X, ldx, n, n, h->vec, h->vec + h->n_max);
+  SDC_LAUNCHED(h);
+  k_norm_finish<<<1, 1024, 0, h->st>>>(h->vec, h->vec + h->n_max, n, out2);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------------------
+// one IRS pass: S holds [B_j; -A_j]; writes A_{j+1}, B_{j+1} and the next stack into S
+// ---------------------------------------------------------------------------------------
+int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double* Bj,
+             long long ldb, double* An, long long ldan, double* Bn, long long ldbn, double* S,
+             int rtest_slot, double* Rout, long long ldr) {
+  const long long m = 2LL * n;
+  SDC_TRY(blocked_qr(h, S, m, (int)m, n, h->Y, m));
+  if (rtest_slot >= 0) {
+    k_rtest_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(S, m, h->Rprev, n, h->vec,
+                                                                  h->vec + h->n_max);
+    SDC_LAUNCHED(h);
+    k_rtest_finish<<<1, 1024, 0, h->st>>>(h->vec, h->vec + h->n_max, n,
+                                          h->scal + SCAL_HIST + rtest_slot);
+    SDC_LAUNCHED(h);
+  }
+  if (Rout) {   // R with non-negative diagonal (test entry point)
+    SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
+    k_rtest_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(S, m, h->Rprev, n, h->vec,
+                                                                  h->vec + h->n_max);
+    SDC_LAUNCHED(h);
+    k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Rout, ldr, h->Rprev, n, n, n, 1.0);
+    SDC_LAUNCHED(h);
+  }
+  // complement [Q12; Q22] = H_0..H_{n-1} [0; I]
+  k_set_zero_identity<<<ew_grid(m * n), 256, 0, h->st>>>(h->C, m, n);
+  SDC_LAUNCHED(h);
+  SDC_TRY(apply_q(h, (int)m, n, h->Y, m, h->C, m, n));
+  // A_{j+1} = Q12^T A_j (-> next stack lower half, negated); B_{j+1} = Q22^T B_j (upper)
+  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, h->C, m, Aj, lda, 0.0, An, ldan, S + n, m, -1.0));
+  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, h->C + n, m, Bj, ldb, 0.0, Bn, ldbn, S, m, 1.0));
+  return 0;
+}
+
+// Q = GRURV(2, A_p+B_p, A_p; -1, +1)   (Alg. 2 with Alg. 1)
+int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* V,
+                long long ldv, double* Q, long long ldq) {
+  const long long ld = n;
+  k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
+  SDC_LAUNCHED(h);                                                     // S = A_p + B_p
+  SDC_TRY(gemm(h, false, true, n, n, n, 1.0, Ap, ld, V, ldv, 0.0, h->G2, ld));  // X = A_p V^T
+  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, h->Y, ld));                   // X = U R_2
+  SDC_TRY(apply_qt(h, n, n, h->Y, ld, h->G1, ld, n));                  // U^T S
+  k_row_sign<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, h->G2, ld, n, n);
+  SDC_LAUNCHED(h);                                                     // U <- U D_U
+  SDC_TRY(transpose_rev(h, h->G3, ld, h->G1, ld, n, 1));               // M = C^T J
+  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, h->Y, ld));                   // M = Q_qr R_qr
+  SDC_TRY(form_q(h, n, h->Y, ld, h->G1, ld));                          // Q_qr explicit
+  k_col_sign_rev<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Q, ldq, h->G1, ld, h->G3, ld, n, 1);
+  SDC_LAUNCHED(h);                                                     // Q = Q_qr D J
+  return 0;
+}
+
+// Q_L = GRURV(2, A'_p^T, (A'_p+B'_p)^T; +1, -1)  (Alg. 4 line 4)
+int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* VL,
+               long long ldv, double* QL, long long ldq) {
+  const long long ld = n;
+  k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
+  SDC_LAUNCHED(h);
+  SDC_TRY(gemm(h, false, true, n, n, n, 1.0, h->G1, ld, VL, ldv, 0.0, h->G2, ld));  // X'
+  SDC_TRY(transpose_rev(h, h->G3, ld, h->G2, ld, n, 2));               // J X' J
+  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, h->Y, ld));                   // = Qt Rt  (QL of X')
+  SDC_TRY(transpose_rev(h, h->G1, ld, Ap, ld, n, 3));                  // J A'_p
+  SDC_TRY(apply_qt(h, n, n, h->Y, ld, h->G1, ld, n));                  // Qt^T J A'_p
+  k_row_sign<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, h->G3, ld, n, n);
+  SDC_LAUNCHED(h);                                                     // D Qt^T J A'_p
+  SDC_TRY(transpose_rev(h, h->G2, ld, h->G1, ld, n, 1));               // Z = A'^T U
+  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, h->Y, ld));
+  SDC_TRY(form_q(h, n, h->Y, ld, h->G1, ld));
+  k_col_sign_rev<<<ew_grid((long long)n * n), 256, 0, h->st>>>(QL, ldq, h->G1, ld, h->G2, ld, n, 0);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+int select_dev(sdc_handle* h, int n, const double* Ah, long long ldah, const double* Bh,
+               long long ldbh, const double* nrmA, const double* nrmB, double* sel) {
+  const int nblk = cdiv(n, SEL_T);
+  ProfScope ps(h, SDC_PROF_SELECT, 8.0 * (double)n * n * (Bh ? 2 : 1));
+  k_select_cols<<<nblk, 256, 0, h->st>>>(Ah, ldah, n, h->pmA);
+  SDC_LAUNCHED(h);
+  if (Bh) {
+    k_select_cols<<<nblk, 256, 0, h->st>>>(Bh, ldbh, n, h->pmB);
+    SDC_LAUNCHED(h);
+  }
+  double* mvals = h->vec + 2 * h->n_max;
+  k_select_rows<<<cdiv(n, 256), 256, 0, h->st>>>(h->pmA, Bh ? h->pmB : nullptr, n, nblk, nrmA,
+                                                 nrmB, mvals);
+  SDC_LAUNCHED(h);
+  k_select_argmin<<<1, 1024, 0, h->st>>>(mvals, n, sel);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+// Ahat = QL^T A Q (+ Bhat), split selection -> scal[4..6]
+int similarity_select(sdc_handle* h, int n, const double* A, long long lda, const double* B,
+                      long long ldb, const double* Q, long long ldq, const double* QL,
+                      long long ldql) {
+  const long long ld = n;
+  SDC_TRY(gemm(h, false, false, n, n, n, 1.0, A, lda, Q, ldq, 0.0, h->T1, ld));
+  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, QL, ldql, h->T1, ld, 0.0, h->Ah, ld));
+  if (B) {
+    SDC_TRY(gemm(h, false, false, n, n, n, 1.0, B, ldb, Q, ldq, 0.0, h->T1, ld));
+    SDC_TRY(gemm(h, true, false, n, n, n, 1.0, QL, ldql, h->T1, ld, 0.0, h->Bh, ld));
+  }
+  SDC_TRY(select_dev(h, n, h->Ah, ld, B ? h->Bh : nullptr, ld, h->scal, h->scal + 2, h->scal + 4));
+  k_e21_fro_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(h->Ah, ld, n, h->scal + 4, h->vec);
+  SDC_LAUNCHED(h);
+  if (B) {
+    k_e21_fro_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(h->Bh, ld, n, h->scal + 4,
+                                                                    h->vec + h->n_max);
+    SDC_LAUNCHED(h);
+  }
+  k_e21_fro_finish<<<1, 1024, 0, h->st>>>(h->vec, B ? h->vec + h->n_max : nullptr, n, h->scal,
+                                          h->scal + 2, h->scal + 6);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+// synchronise and report a grid-barrier timeout recorded by a panel kernel (bar[1])
+int check_barrier(sdc_handle* h) {
+  unsigned int err = 0;
+  SDC_CK(cudaMemcpyAsync(&err, h->bar + 1, sizeof(err), cudaMemcpyDeviceToHost, h->st));
+  SDC_CK(cudaStreamSynchronize(h->st));
+  if (err) {
+    set_err("panel grid barrier timed out (co-residency violated?)");
+    return SDC_ERR_CUDA;
+  }
+  return 0;
+}
+
+int check_handle(sdc_handle* h) {
+  if (!h) {
+    set_err("null handle");
+    return -1;
+  }
+  int dev = -1;
+  SDC_CK(cudaGetDevice(&dev));
+  if (dev != h->device) SDC_CK(cudaSetDevice(h->device));
+  return 0;
+}
+
+}  // namespace
+
+// =======================================================================================
+// C ABI
+// =======================================================================================
+extern "C" {
+
+const char* sdc_last_error(void) { return g_err; }
+
+long long sdc_kernel_launches(const sdc_handle* h) { return h ? h->launches : 0; }
+
+int sdc_profile(sdc_handle* h, int enable) {
+  if (!h) return -1;
+  prof_collect(h);
+  h->prof_on = enable != 0;
+  for (int c = 0; c < SDC_PROF_CLASSES; ++c) { h->prof_ms[c] = 0; h->prof_work[c] = 0; h->prof_n[c] = 0; }
+  return 0;
+}
+
+int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, double* work) {
+  if (!h) return -1;
+  if (cls < 0 || cls >= SDC_PROF_CLASSES) return -2;
+  prof_collect(h);
+  if (ms) *ms = h->prof_ms[cls];
+  if (launches) *launches = h->prof_n[cls];
+  if (work) *work = h->prof_work[cls];
+  return 0;
+}
+
+void sdc_destroy(sdc_handle* h) {
+  if (!h) return;
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (void* p : h->allocs) cudaFree(p);
+  delete h;
+}
+
+int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
+  if (!out) { set_err("sdc_create: null output"); return -1; }
+  *out = nullptr;
+  if (n_max < 2 || n_max > 24576) { set_err("sdc_create: n_max %d out of [2, 24576]", n_max); return -3; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_err("sdc_create: no CUDA device (no CPU fallback)");
+    return SDC_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) { set_err("sdc_create: bad device %d", device); return -2; }
+  SDC_CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  SDC_CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    set_err("sdc_create: device is sm_%d%d; libsdc is built for sm_100a only", prop.major, prop.minor);
+    return SDC_ERR_NOT_SUPPORTED;
+  }
+  int coop = 0;
+  SDC_CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) { set_err("sdc_create: cooperative launch unsupported"); return SDC_ERR_NOT_SUPPORTED; }
+  sdc_handle* h = new sdc_handle();
+  h->device = device;
+  h->n_max = n_max;
+  h->pencil = pencil ? 1 : 0;
+  h->num_sms = prop.multiProcessorCount;
+  const size_t n = (size_t)n_max, nn = n * n;
+  int rc = 0;
+#define ALLOC(p, e) \
+  if (!rc) rc = dalloc(h, &(p), (e))
+  ALLOC(h->S, 2 * nn);
+  ALLOC(h->Y, 2 * nn);
+  ALLOC(h->C, 2 * nn);
+  ALLOC(h->A[0], nn); ALLOC(h->A[1], nn); ALLOC(h->B[0], nn); ALLOC(h->B[1], nn);
+  ALLOC(h->G1, nn); ALLOC(h->G2, nn); ALLOC(h->G3, nn); ALLOC(h->T1, nn); ALLOC(h->Ah, nn);
+  ALLOC(h->Rprev, nn);
+  if (h->pencil) {
+    ALLOC(h->SL, 2 * nn);
+    ALLOC(h->AL[0], nn); ALLOC(h->AL[1], nn); ALLOC(h->BL[0], nn); ALLOC(h->BL[1], nn);
+    ALLOC(h->Bh, nn); ALLOC(h->QLb, nn);
+  }
+  ALLOC(h->Tb, (n / NB + 1) * NB * NB);
+  ALLOC(h->tau, n + NB);
+  h->wp_elems = (size_t)NB * (2 * (size_t)h->num_sms * TileM::BN + 2 * n + 256);
+  ALLOC(h->Wp, h->wp_elems);
+  ALLOC(h->W, (size_t)NB * (n + 64));
+  ALLOC(h->gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
+  ALLOC(h->pmA, (n / SEL_T + 1) * n);
+  if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
+  ALLOC(h->vec, 4 * n + 64);
+  ALLOC(h->scal, SCAL_HIST + MAX_HIST);
+#undef ALLOC
+  if (!rc) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, 64);
+    if (e != cudaSuccess) { set_err("cudaMalloc: %s", cudaGetErrorString(e)); rc = SDC_ERR_NOMEM; }
+    else { h->allocs.push_back(q); h->bar = (unsigned*)q; h->flag = (int*)((char*)q + 32); }
+  }
+  if (rc) { sdc_destroy(h); return rc; }
+  *out = h;
+  return 0;
+}
+
+int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+              int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
+              int max_iters, double tol, int stop_mode, double* Q, int ldq, double* QL, int ldql,
+              double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res) {
+  SDC_TRY(check_handle(h));
+  if (n < 2 || n > h->n_max) { set_err("n=%d outside [2, n_max=%d]", n, h->n_max); return -3; }
+  if (!A) { set_err("A is NULL"); return -4; }
+  if (lda < n) { set_err("lda < n"); return -5; }
+  const bool pencil = B != nullptr;
+  if (pencil && ldb < n) { set_err("ldb < n"); return -7; }
+  if (pencil && !h->pencil) { set_err("handle created without pencil workspace"); return -6; }
+  if (!V) { set_err("V is NULL"); return -8; }
+  if (ldv < n) { set_err("ldv < n"); return -9; }
+  if (pencil && !VL) { set_err("VL is NULL for a pencil"); return -10; }
+  if (pencil && ldvl < n) { set_err("ldvl < n"); return -11; }
+  if (region != SDC_REGION_UNIT_DISK) { set_err("unknown region %d", region); return -12; }
+  if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -13; }
+  if (!(tol >= 0.0)) { set_err("tol < 0"); return -14; }
+  if (stop_mode < 0 || stop_mode > 2) { set_err("unknown stop mode"); return -15; }
+  if (!Q) { set_err("Q is NULL"); return -16; }
+  if (ldq < n) { set_err("ldq < n"); return -17; }
+  if (pencil && !QL) { set_err("QL is NULL for a pencil"); return -18; }
+  if (QL && ldql < n) { set_err("ldql < n"); return -19; }
+  if (Ahat && ldah < n) { set_err("ldah < n"); return -21; }
+  if (hist_cap < 0 || (hist_cap > 0 && !hist)) { set_err("bad hist"); return -23; }
+  if (!res) { set_err("res is NULL"); return -24; }
+  h->st = static_cast<cudaStream_t>(stream);
+  const long long ld = n, m = 2LL * n;
+
+  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
+  h->bar_count = 0;
+  SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
+  SDC_TRY(norms(h, A, lda, n, h->scal));
+  if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
+  // A_0 = A, B_0 = B (or I); stack S = [B_0; -A_0]
+  k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->A[0], ld, A, lda, n, n, 1.0);
+  SDC_LAUNCHED(h);
+  if (pencil) k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, 1.0);
+  else k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, 1.0);
+  SDC_LAUNCHED(h);
+  k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
+  SDC_LAUNCHED(h);
+  if (pencil) {   // left IRS on (A^T, B^T)
+    SDC_TRY(transpose_rev(h, h->AL[0], ld, A, lda, n, 0));
+    SDC_TRY(transpose_rev(h, h->BL[0], ld, B, ldb, n, 0));
+    k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->SL, m, h->AL[0], ld, h->BL[0], ld, n);
+    SDC_LAUNCHED(h);
+  }
+  double* QLd = pencil ? h->QLb : nullptr;
+  std::vector<double> hbuf;
+  if (hist_cap > 0) hbuf.assign((size_t)hist_cap * 3, NAN);
+
+  int cur = 0, p = max_iters, conv = 0;
+  bool have_split = false;
+  double hsel[8];
+  for (int j = 0; j < max_iters; ++j) {
+    SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S,
+                     j, nullptr, 0));
+    if (pencil)
+      SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
+                       h->SL, -1, nullptr, 0));
+    cur ^= 1;
+    if (stop_mode == SDC_STOP_RTEST && j >= 1) {
+      double ratio;
+      SDC_CK(cudaMemcpyAsync(&ratio, h->scal + SCAL_HIST + j, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      SDC_CK(cudaStreamSynchronize(h->st));
+      if (ratio <= tol) { p = j + 1; conv = 1; break; }
+    }
+    if (stop_mode == SDC_STOP_E21) {
+      SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], V, ldv, Q, ldq));
+      if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], VL, ldvl, QLd, ld));
+      SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
+      have_split = true;
+      SDC_CK(cudaMemcpyAsync(hsel, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      SDC_CK(cudaStreamSynchronize(h->st));
+      if (j < hist_cap) { hbuf[3 * j] = hsel[0]; hbuf[3 * j + 1] = hsel[1]; }
+      if (hsel[1] <= tol) { p = j + 1; conv = 1; break; }
+    }
+  }
+  if (!have_split) {
+    SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], V, ldv, Q, ldq));
+    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], VL, ldvl, QLd, ld));
+    SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
+  }
+  SDC_CK(cudaMemsetAsync(h->flag, 0, sizeof(int), h->st));
+  k_nonfinite<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->Ah, ld, n, h->flag);
+  SDC_LAUNCHED(h);
+  if (pencil) SDC_CK(cudaMemcpy2DAsync(QL, sizeof(double) * ldql, QLd, sizeof(double) * ld,
+                                       sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
+  if (Ahat) SDC_CK(cudaMemcpy2DAsync(Ahat, sizeof(double) * ldah, h->Ah, sizeof(double) * ld,
+                                     sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
+  std::vector<double> sc(SCAL_HIST + (size_t)max_iters);
+  int flag = 0;
+  SDC_CK(cudaMemcpyAsync(sc.data(), h->scal, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, h->st));
+  SDC_CK(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  SDC_TRY(check_barrier(h));
+  for (int j = 1; j < std::min(hist_cap, p); ++j) hbuf[3 * j + 2] = sc[SCAL_HIST + j];
+  if (hist_cap > 0) memcpy(hist, hbuf.data(), sizeof(double) * hbuf.size());
+  res->r = (int)sc[4];
+  res->k = n - res->r;
+  res->metric = sc[5];
+  res->metric_fro = sc[6];
+  res->iters = p;
+  res->converged = conv;
+  res->status = (flag || !std::isfinite(res->metric)) ? SDC_STATUS_NONFINITE
+               : (res->metric <= SDC_SPLIT_ACCEPT ? SDC_STATUS_SPLIT : SDC_STATUS_NO_SPLIT);
+  return 0;
+}
+
+int sdc_split_host(sdc_handle* h, void* stream, int n, const double* A, const double* B,
+                   const double* V, const double* VL, int max_iters, double tol, int stop_mode,
+                   double* Q, double* QL, double* Ahat, double* hist, int hist_cap,
+                   sdc_result* res) {
+  SDC_TRY(check_handle(h));
+  if (n < 2 || n > h->n_max) { set_err("n=%d outside [2, n_max=%d]", n, h->n_max); return -3; }
+  if (!A || !V || !Q || (B && !VL) || (B && !QL)) { set_err("null host pointer"); return -4; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t nn = (size_t)h->n_max * h->n_max, bytes = sizeof(double) * (size_t)n * n;
+  int rc = 0;
+  if (!h->hA) { rc = dalloc(h, &h->hA, nn); if (!rc) rc = dalloc(h, &h->hV, nn); if (!rc) rc = dalloc(h, &h->hQ, nn); }
+  if (!rc && B && !h->hB) { rc = dalloc(h, &h->hB, nn); if (!rc) rc = dalloc(h, &h->hVL, nn); if (!rc) rc = dalloc(h, &h->hQL, nn); }
+  if (!rc && Ahat && !h->hAh) rc = dalloc(h, &h->hAh, nn);
+  if (rc) return rc;
+  SDC_CK(cudaMemcpyAsync(h->hA, A, bytes, cudaMemcpyHostToDevice, st));
+  SDC_CK(cudaMemcpyAsync(h->hV, V, bytes, cudaMemcpyHostToDevice, st));
+  if (B) {
+    SDC_CK(cudaMemcpyAsync(h->hB, B, bytes, cudaMemcpyHostToDevice, st));
+    SDC_CK(cudaMemcpyAsync(h->hVL, VL, bytes, cudaMemcpyHostToDevice, st));
+  }
+  SDC_TRY(sdc_split(h, stream, n, h->hA, n, B ? h->hB : nullptr, n, h->hV, n, B ? h->hVL : nullptr, n,
+                    SDC_REGION_UNIT_DISK, max_iters, tol, stop_mode, h->hQ, n, B ? h->hQL : nullptr, n,
+                    Ahat ? h->hAh : nullptr, n, hist, hist_cap, res));
+  SDC_CK(cudaMemcpyAsync(Q, h->hQ, bytes, cudaMemcpyDeviceToHost, st));
+  if (B) SDC_CK(cudaMemcpyAsync(QL, h->hQL, bytes, cudaMemcpyDeviceToHost, st));
+  if (Ahat) SDC_CK(cudaMemcpyAsync(Ahat, h->hAh, bytes, cudaMemcpyDeviceToHost, st));
+  SDC_CK(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N, int K,
+              double alpha, const double* A, int lda, const double* B, int ldb, double beta,
+              double* C, int ldc) {
+  SDC_TRY(check_handle(h));
+  if (M < 0) { set_err("invalid argument (M < 0)"); return -5; }
+  if (N < 0) { set_err("invalid argument (N < 0)"); return -6; }
+  if (K < 0) { set_err("invalid argument (K < 0)"); return -7; }
+  if (lda < std::max(1, transa ? K : M)) { set_err("invalid argument (lda < std::max(1, transa ? K : M))"); return -10; }
+  if (ldb < std::max(1, transb ? N : K)) { set_err("invalid argument (ldb < std::max(1, transb ? N : K))"); return -12; }
+  if (ldc < std::max(1, M)) { set_err("invalid argument (ldc < std::max(1, M))"); return -15; }
+  h->st = static_cast<cudaStream_t>(stream);
+  return gemm(h, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double* Qthin, int ldq) {
+  SDC_TRY(check_handle(h));
+  if (m < n || m > 2 * h->n_max) { set_err("invalid argument (m < n || m > 2 * h->n_max)"); return -3; }
+  if (n < 1 || n > h->n_max) { set_err("invalid argument (n < 1 || n > h->n_max)"); return -4; }
+  if (lda < m) { set_err("invalid argument (lda < m)"); return -6; }
+  if (Qthin && ldq < m) { set_err("invalid argument (Qthin && ldq < m)"); return -8; }
+  h->st = static_cast<cudaStream_t>(stream);
+  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
+  h->bar_count = 0;
+  SDC_TRY(blocked_qr(h, A, lda, m, n, h->Y, m));
+  if (Qthin) {
+    k_set_identity<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, 1.0);
+    SDC_LAUNCHED(h);
+    SDC_TRY(apply_q(h, m, n, h->Y, m, Qthin, ldq, n));
+    k_col_sign<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, A, lda);
+    SDC_LAUNCHED(h);
+  }
+  SDC_TRY(check_barrier(h));
+  return 0;
+}
+
+int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+                 int ldb, double* Aout, int ldao, double* Bout, int ldbo, double* Rout, int ldr) {
+  SDC_TRY(check_handle(h));
+  if (n < 1 || n > h->n_max) { set_err("invalid argument (n < 1 || n > h->n_max)"); return -3; }
+  if (!A || lda < n) { set_err("invalid argument (!A || lda < n)"); return -4; }
+  if (!B || ldb < n) { set_err("invalid argument (!B || ldb < n)"); return -6; }
+  if (!Aout || ldao < n) { set_err("invalid argument (!Aout || ldao < n)"); return -8; }
+  if (!Bout || ldbo < n) { set_err("invalid argument (!Bout || ldbo < n)"); return -10; }
+  if (Rout && ldr < n) { set_err("invalid argument (Rout && ldr < n)"); return -13; }
+  h->st = static_cast<cudaStream_t>(stream);
+  const long long m = 2LL * n;
+  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
+  h->bar_count = 0;
+  k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, A, lda, B, ldb, n);
+  SDC_LAUNCHED(h);
+  SDC_TRY(irs_pass(h, n, A, lda, B, ldb, Aout, ldao, Bout, ldbo, h->S, -1, Rout, ldr));
+  SDC_TRY(check_barrier(h));
+  return 0;
+}
+
+int sdc_split_select(sdc_handle* h, void* stream, int n, const double* Ahat, int ldah,
+                     double normA, const double* Bhat, int ldbh, double normB, int* r,
+                     double* metric, double* mvals) {
+  SDC_TRY(check_handle(h));
+  if (n < 2 || n > h->n_max) { set_err("invalid argument (n < 2 || n > h->n_max)"); return -3; }
+  if (!Ahat || ldah < n) { set_err("invalid argument (!Ahat || ldah < n)"); return -4; }
+  if (Bhat && (ldbh < n || !h->pencil)) { set_err("invalid argument (Bhat && (ldbh < n || !h->pencil))"); return -7; }
+  if (!r || !metric) { set_err("invalid argument (!r || !metric)"); return -10; }
+  h->st = static_cast<cudaStream_t>(stream);
+  double nr[4] = {normA, 0.0, normB, 0.0};
+  SDC_CK(cudaMemcpyAsync(h->scal, nr, sizeof(nr), cudaMemcpyHostToDevice, h->st));
+  SDC_TRY(select_dev(h, n, Ahat, ldah, Bhat, ldbh, h->scal, h->scal + 2, h->scal + 4));
+  double sel[2];
+  SDC_CK(cudaMemcpyAsync(sel, h->scal + 4, sizeof(sel), cudaMemcpyDeviceToHost, h->st));
+  if (mvals)
+    SDC_CK(cudaMemcpyAsync(mvals, h->vec + 2 * h->n_max, sizeof(double) * n, cudaMemcpyDeviceToDevice, h->st));
+  SDC_CK(cudaStreamSynchronize(h->st));
+  *r = (int)sel[0];
+  *metric = sel[1];
+  return 0;
+}
+
+}  // extern "C"
