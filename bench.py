@@ -224,7 +224,7 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     launches = (h.launches - launches0) // args.steps
-    prof = {c: h.profile_read(c) for c in range(4)}
+    prof = {c: h.profile_read(c) for c in range(7)}
     h.profile(False)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -288,8 +288,10 @@ def main():
              "launches_per_step": p_n // max(1, args.steps)}
     if panel["achieved"]:
         panel["frac"] = panel["achieved"] / hbm
-    others = {name: {"ms_per_step": prof[c][0] / args.steps, "launches_per_step": prof[c][1] // args.steps}
-              for c, name in ((2, "k_wy_reduce"), (3, "split_select"))}
+    others = {name: {"ms_per_step": prof[c][0] / args.steps, "launches_per_step": prof[c][1] // args.steps,
+                     "tflops": (prof[c][2] / (prof[c][0] / 1e3) / 1e12) if (c >= 4 and prof[c][0] > 0) else None}
+              for c, name in ((2, "k_wy_reduce"), (3, "split_select"), (4, "gemm W0=Y^T C (split-K)"),
+                              (5, "gemm rank-nb update C-=YW"), (6, "gemm n x n products"))}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -137,8 +137,12 @@ int sdc_split_select(sdc_handle* h, void* stream, int n, const double* Ahat, int
  * sdc_profile_read returns, for class cls, the summed event time (ms), the number of
  * launches and the summed ALGORITHMIC work: flops 2MNK for SDC_PROF_GEMM, bytes
  * (read + write of the operands the definition touches) for the other classes. */
-enum { SDC_PROF_GEMM = 0, SDC_PROF_PANEL = 1, SDC_PROF_WYRED = 2, SDC_PROF_SELECT = 3,
-       SDC_PROF_CLASSES = 4 };
+enum { SDC_PROF_GEMM = 0,        /* every DMMA GEMM launch                                */
+       SDC_PROF_PANEL = 1, SDC_PROF_WYRED = 2, SDC_PROF_SELECT = 3,
+       SDC_PROF_GEMM_W0 = 4,     /* subset of GEMM: split-K W0 = Y^T C of WY applications    */
+       SDC_PROF_GEMM_UPD = 5,    /* subset of GEMM: rank-nb updates C -= Y W                 */
+       SDC_PROF_GEMM_OTHER = 6,  /* subset of GEMM: the n x n products (a5, a7, a8)         */
+       SDC_PROF_CLASSES = 7 };
 int sdc_profile(sdc_handle* h, int enable);
 int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, double* work);
 

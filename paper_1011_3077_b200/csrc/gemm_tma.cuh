@@ -1,0 +1,200 @@
+// gemm_tma.cuh -- warp-specialised FP64 tensor-core GEMM for sm_100a, TMA-fed.
+//
+//   C[z] (M x N) = alpha * A^T B [K-slice z] + beta * C[z]    ("TN": both operands K-major)
+//   optional second output  D2 = alpha2 * A^T B               (dual epilogue)
+//
+// A is stored K x M column-major (ld lda), B is stored K x N column-major (ld ldb), so
+// both tiles are K-contiguous; every contraction of the split step is written in this
+// form: W0 = Y^T C, C -= (Y^T)^T W, Q12^T A_j, (A_p^T)^T (V^T), A^T Q, G^T Q.
+//
+// Pipeline: lane 0 of warp 0 streams 16-deep K slices of the A and B tiles into a
+// STAGES-deep shared-memory ring with TMA (cp.async.bulk.tensor.2d, 128-byte swizzle, zero
+// fill outside the tensor -> ragged edges need no code), completion tracked by mbarrier
+// transaction counts; every warp waits on the slot's "full" barrier, runs
+// mma.sync.m8n8k4.f64 (DMMA) on register accumulators and releases the slot through its
+// "empty" barrier, which the issuing lane waits on before refilling it.  No
+// __syncthreads in the main loop, no per-thread address math.  (A dedicated producer warp
+// would put 3 warps on one SM sub-partition and cap the accumulator registers at 168.)
+//
+// Bank conflicts: with the 128B swizzle, element (row, k) of a 16-wide K slice lives at
+// double index row*16 + ((k/2 XOR row%8)*2 + k%2).  A DMMA fragment's half-warp reads 4
+// rows x 4 k; mapping fragment row r (0..7) to tile row 2*(r%4) + r/4 makes the 4 rows of a
+// half-warp {0,2,4,6} (or {1,3,5,7}) and the 16 addresses distinct mod 16 doubles.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace sdc {
+
+struct TmaGemmArgs {
+  int M, N, K;
+  double* C; long long ldc;
+  double alpha, beta;
+  double* D2; long long ldd2; double alpha2;
+  int kchunk;             // K per z-slice (multiple of 16)
+  long long c_zstride;    // element stride between z-slices of C
+};
+
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1>
+struct TmaTile {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BK = 16;                       // one 128-byte swizzle row of doubles
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int CWARPS = WARPS_M * WARPS_N;    // all warps consume
+  static constexpr int THREADS = CWARPS * 32;
+  static constexpr int MI = WM / 8, NI = WN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+};
+
+SDC_DEV void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+SDC_DEV void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+SDC_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+SDC_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+SDC_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+SDC_DEV int frag_row(int r) { return 2 * (r & 3) + (r >> 2); }   // conflict-free row map
+SDC_DEV int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
+
+template <class T>
+__global__ void __launch_bounds__(T::THREADS, T::MINB)
+gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const TmaGemmArgs g) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  uint64_t* empty = full + T::STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * T::BM, n0 = blockIdx.y * T::BN;
+  const int kbeg = blockIdx.z * g.kchunk;
+  const int kend = min(g.K, kbeg + g.kchunk);
+  const int ktiles = kend > kbeg ? (kend - kbeg + T::BK - 1) / T::BK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < T::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, T::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // stage issue (one lane): tile kt -> slot kt % STAGES, after the slot's previous use
+  auto issue = [&](int kt) {
+    const int s = kt % T::STAGES;
+    if (kt >= T::STAGES) mbar_wait(empty + s, ((kt / T::STAGES) - 1) & 1);
+    unsigned char* st = base + (size_t)s * T::STAGE_BYTES;
+    mbar_expect_tx(full + s, T::STAGE_BYTES);
+    const int k = kbeg + kt * T::BK;
+    tma_load_2d(st, &tmA, k, m0, full + s);
+    tma_load_2d(st + T::A_BYTES, &tmB, k, n0, full + s);
+  };
+  if (g.beta != 0.0) {   // warm L2 with this CTA's C tile: one prefetch per 128-byte line
+    const double* Cz = g.C + (long long)blockIdx.z * g.c_zstride;
+    constexpr int LPC = (T::BM * 8 + 127) / 128;            // lines per column
+    for (int e = threadIdx.x; e < LPC * T::BN; e += T::THREADS) {
+      const int n = n0 + e / LPC, m = m0 + (e % LPC) * 16;
+      if (n < g.N && m < g.M)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(Cz + m + (long long)n * g.ldc));
+    }
+  }
+  const bool producer = (threadIdx.x == 0);
+  if (producer)
+    for (int kt = 0; kt < min(ktiles, T::STAGES - 1); ++kt) issue(kt);
+
+  // ---- consumers ----
+  const int wm = warp % T::WARPS_M, wn = warp / T::WARPS_M;
+  double acc[T::MI][T::NI][2];
+#pragma unroll
+  for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < T::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int fr = frag_row(lane >> 2), fc = lane & 3;
+  int aoff[T::MI], boff[T::NI];       // fragment row offsets within the stage tile
+#pragma unroll
+  for (int i = 0; i < T::MI; ++i) aoff[i] = wm * T::WM + i * 8 + fr;
+#pragma unroll
+  for (int j = 0; j < T::NI; ++j) boff[j] = wn * T::WN + j * 8 + fr;
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % T::STAGES;
+    if (producer && kt + T::STAGES - 1 < ktiles) issue(kt + T::STAGES - 1);
+    mbar_wait(full + s, (kt / T::STAGES) & 1);
+    const double* sA = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES);
+    const double* sB = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES + T::A_BYTES);
+#pragma unroll
+    for (int kk = 0; kk < T::BK; kk += 4) {
+      double af[T::MI], bf[T::NI];
+#pragma unroll
+      for (int i = 0; i < T::MI; ++i) af[i] = sA[swz(aoff[i], kk + fc)];
+#pragma unroll
+      for (int j = 0; j < T::NI; ++j) bf[j] = sB[swz(boff[j], kk + fc)];
+#pragma unroll
+      for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + s);
+  }
+
+  // ---- epilogue: C = alpha acc + beta C (C prefetched into L2 at kernel start) ----------
+  double* __restrict__ C = g.C + (long long)blockIdx.z * g.c_zstride;
+  double* __restrict__ D2 = g.D2;
+  const int c0 = frag_row(2 * fc), c1 = frag_row(2 * fc + 1);
+  const bool use_beta = g.beta != 0.0;
+#pragma unroll
+  for (int i = 0; i < T::MI; ++i) {
+    const int m = m0 + aoff[i];
+    const bool mok = m < g.M;
+    double old[T::NI][2];
+    if (use_beta) {          // issue this row-fragment's loads together (MLP), then update
+#pragma unroll
+      for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = n0 + wn * T::WN + j * 8 + (h ? c1 : c0);
+          old[j][h] = (mok && n < g.N) ? C[m + (long long)n * g.ldc] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn * T::WN + j * 8 + (h ? c1 : c0);
+        if (!mok || n >= g.N) continue;
+        const double v = acc[i][j][h];
+        double out = g.alpha * v;
+        if (use_beta) out = fma(g.beta, old[j][h], out);
+        C[m + (long long)n * g.ldc] = out;
+        if (D2) D2[m + (long long)n * g.ldd2] = g.alpha2 * v;
+      }
+  }
+}
+
+}  // namespace sdc

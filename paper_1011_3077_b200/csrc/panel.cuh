@@ -31,6 +31,7 @@ struct PanelArgs {
   double* P; long long ldp;   // panel (m x nb), factored in place (R upper, v below)
   int m, nb;                  // rows, columns (nb <= PANEL_NB, m >= nb)
   double* Y; long long ldy;   // out: explicit Y (m x nb): 0 above diag, 1 on diag, v below
+  double* Yt; long long ldyt; // out: Y^T (nb x m), the K-major operand of C -= Y W
   double* T;                  // out: nb x nb upper-triangular T (ld nb), I - Y T Y^T = H_0..H_{nb-1}
   double* tau;                // out: nb
   double* gbuf;               // workspace: 2 * (gridDim.x + 1) * PANEL_NB doubles
@@ -158,6 +159,12 @@ panel_qr_kernel(const PanelArgs a) {
     double v = Ps[r * PANEL_LD + j];
     a.P[(long long)gr + (long long)j * a.ldp] = v;
     a.Y[(long long)gr + (long long)j * a.ldy] = gr > j ? v : (gr == j ? 1.0 : 0.0);
+  }
+  for (int e = tid; e < R * nb; e += PANEL_THREADS) {     // Y^T: contiguous along j
+    int r = e / nb, j = e % nb;
+    int gr = r0 + r;
+    double v = Ps[r * PANEL_LD + j];
+    a.Yt[(long long)j + (long long)gr * a.ldyt] = gr > j ? v : (gr == j ? 1.0 : 0.0);
   }
   if (cta == 0)
     for (int e = tid; e < nb * nb; e += PANEL_THREADS) {

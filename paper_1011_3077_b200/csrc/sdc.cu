@@ -10,9 +10,12 @@
 //   GRURV (Alg. 1/2):  X = A_p V^T, QR(X) -> U, C = U^T (A_p+B_p), RQ(C) computed as the
 //     QR of C^T J with explicit Q, Q = Q_qr D J (reading Q10).
 //   Similarity Q_L^T A Q and split selection.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -23,6 +26,7 @@
 #include "aux.cuh"
 #include "common.cuh"
 #include "gemm.cuh"
+#include "gemm_tma.cuh"
 #include "panel.cuh"
 
 using namespace sdc;
@@ -62,7 +66,8 @@ struct sdc_handle {
   int device = 0, n_max = 0, pencil = 0, num_sms = 0;
   cudaStream_t st = nullptr;
   // workspace (see sdc_create for sizes)
-  double *S = nullptr, *SL = nullptr, *Y = nullptr, *C = nullptr;
+  double *S = nullptr, *SL = nullptr, *Y = nullptr, *Yt = nullptr, *C = nullptr;
+  double *Vt = nullptr, *VLt = nullptr;
   double *A[2] = {nullptr, nullptr}, *B[2] = {nullptr, nullptr};
   double *AL[2] = {nullptr, nullptr}, *BL[2] = {nullptr, nullptr};
   double *G1 = nullptr, *G2 = nullptr, *G3 = nullptr, *T1 = nullptr, *Ah = nullptr, *Bh = nullptr;
@@ -76,6 +81,7 @@ struct sdc_handle {
   long long launches = 0;
   // optional per-kernel-class timing with CUDA events on the launching stream
   bool prof_on = false;
+  int gemm_sub = SDC_PROF_GEMM_OTHER;   // sub-class of the GEMMs being launched
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   struct ProfRec { int cls; int e0, e1; double work; };
@@ -130,14 +136,18 @@ int prof_event(sdc_handle* h) {
   return id;
 }
 struct ProfScope {
-  sdc_handle* h; int cls; double work; int e0;
-  ProfScope(sdc_handle* h_, int cls_, double work_) : h(h_), cls(cls_), work(work_), e0(-1) {
+  sdc_handle* h; int cls, sub; double work; int e0;
+  ProfScope(sdc_handle* h_, int cls_, double work_, int sub_ = -1)
+      : h(h_), cls(cls_), sub(sub_), work(work_), e0(-1) {
     if (h->prof_on) e0 = prof_event(h);
   }
   ~ProfScope() {
     if (h->prof_on && e0 >= 0) {
       int e1 = prof_event(h);
-      if (e1 >= 0) h->recs.push_back({cls, e0, e1, work});
+      if (e1 >= 0) {
+        h->recs.push_back({cls, e0, e1, work});
+        if (sub >= 0) h->recs.push_back({sub, e0, e1, work});
+      }
     }
   }
 };
@@ -156,11 +166,19 @@ void prof_collect(sdc_handle* h) {
 }
 
 // ---------------------------------------------------------------------------------------
-// GEMM dispatch
+// GEMM dispatch.  Every contraction of the step is TN (both operands K-major):
+//   C = alpha A_s^T B_s + beta C, A_s K x M, B_s K x N (column-major).
+// TMA path (gemm_tma.cuh) when both operands are 16-byte aligned with even ld; otherwise
+// the cp.async kernel (gemm.cuh) -- same arithmetic, only the operand staging differs.
 // ---------------------------------------------------------------------------------------
-using TileL = GemmTile<128, 128, 16, 64, 32, 4>;  // 8 warps, warp tile 64x32
-using TileM = GemmTile<64, 128, 16, 32, 32, 4>;   // 8 warps (W0 = Y^T C, M = nb)
-using TileS = GemmTile<64, 64, 16, 32, 32, 4>;    // 4 warps (small problems)
+using TileL = GemmTile<128, 128, 16, 64, 32, 4>;  // cp.async fallback tiles
+using TileM = GemmTile<64, 128, 16, 32, 32, 4>;
+using TileS = GemmTile<64, 64, 16, 32, 32, 4>;
+
+using TmaL = TmaTile<128, 128, 64, 32, 6>;      // 8 consumer warps, 192 KB ring
+using TmaM = TmaTile<64, 128, 32, 32, 6>;       // M <= 64 (W0 = Y^T C), 8 consumer warps
+using TmaS = TmaTile<64, 64, 32, 32, 6>;        // small grids, 4 consumer warps
+using TmaU = TmaTile<128, 64, 64, 32, 4, 2>;    // rank-nb updates: 2 CTAs/SM, epilogue overlap
 
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
@@ -172,7 +190,7 @@ int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
     attr_set = 1;
   }
   dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
-  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K);
+  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
   gemm_dmma_kernel<T, TA, TB, VEC><<<grid, T::THREADS, Sm::BYTES, h->st>>>(g);
   SDC_LAUNCHED(h);
   return 0;
@@ -192,28 +210,128 @@ int launch_gemm_tile(sdc_handle* h, const GemmArgs& g, int splits) {
   return launch_gemm_v<TileS, TA, TB>(h, g, splits);
 }
 
-// C = alpha op(A) op(B) + beta C  [+ D2 = alpha2 op(A) op(B)]
-int gemm(sdc_handle* h, bool ta, bool tb, int M, int N, int K, double alpha, const double* A,
-         long long lda, const double* B, long long ldb, double beta, double* C, long long ldc,
-         double* D2 = nullptr, long long ldd2 = 0, double alpha2 = 0.0) {
+// ---- TMA descriptors (driver entry point fetched once through the runtime) ----------
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// 2-D fp64 K-major operand: rows = K (contiguous), cols = M or N, ld in elements.
+// Box = 16 (one 128-byte swizzle row) x box_cols; zero fill outside the tensor.
+bool make_tmap(CUtensorMap* tm, const double* ptr, int rows, int cols, long long ld, int box_cols) {
+  auto fn = tma_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_cols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int gemm_variant_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SDC_GEMM_VARIANT");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+template <class T>
+int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
+                 const TmaGemmArgs& g, int splits) {
+  static int attr_set = 0;
+  if (!attr_set) {
+    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)T::SMEM));
+    attr_set = 1;
+  }
+  CUtensorMap tA, tB;
+  if (!make_tmap(&tA, A, g.K, g.M, lda, T::BM) || !make_tmap(&tB, B, g.K, g.N, ldb, T::BN)) {
+    set_err("cuTensorMapEncodeTiled failed");
+    return SDC_ERR_CUDA;
+  }
+  dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
+  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
+  gemm_tn_tma_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, g);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+// C = alpha A_s^T B_s + beta C  [+ D2 = alpha2 A_s^T B_s];  K-split into `splits` slices of
+// kchunk (multiple of 16) written to C + z * c_zstride when splits > 1.
+int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, long long lda,
+            const double* B, long long ldb, double beta, double* C, long long ldc,
+            double* D2 = nullptr, long long ldd2 = 0, double alpha2 = 0.0, int splits = 1,
+            int kchunk = 0, long long c_zstride = 0) {
   if (M <= 0 || N <= 0) return 0;
-  GemmArgs g{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, D2, ldd2, alpha2, std::max(K, 1), 0};
+  if (splits <= 1) { splits = 1; kchunk = std::max(K, 1); }
+  const bool tma = K > 0 && al16(A, lda) && al16(B, ldb) && tma_encode_fn() != nullptr;
+  if (tma) {
+    TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride};
+    int v = gemm_variant_override();
+    if (v < 0) {
+      if (M <= 64) v = 1;
+      else if (K <= 128) v = 3;
+      else if ((long long)cdiv(M, 128) * cdiv(N, 128) * splits >= h->num_sms) v = 0;
+      else v = 2;
+    }
+    switch (v) {
+      case 0: return launch_tma_t<TmaL>(h, A, lda, B, ldb, g, splits);
+      case 1: return launch_tma_t<TmaM>(h, A, lda, B, ldb, g, splits);
+      case 2: return launch_tma_t<TmaS>(h, A, lda, B, ldb, g, splits);
+      default: return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
+    }
+  }
+  GemmArgs g{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride};
+  return launch_gemm_tile<true, false>(h, g, splits);
+}
+
+// general op(A) op(B) (test entry point sdc_dgemm only; the step itself is all-TN)
+int gemm_general(sdc_handle* h, bool ta, bool tb, int M, int N, int K, double alpha,
+                 const double* A, long long lda, const double* B, long long ldb, double beta,
+                 double* C, long long ldc) {
+  if (M <= 0 || N <= 0) return 0;
+  if (ta && !tb) return gemm_tn(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  GemmArgs g{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, nullptr, 0, 0.0, std::max(K, 1), 0};
   if (!ta && !tb) return launch_gemm_tile<false, false>(h, g, 1);
-  if (ta && !tb) return launch_gemm_tile<true, false>(h, g, 1);
   if (!ta && tb) return launch_gemm_tile<false, true>(h, g, 1);
   return launch_gemm_tile<true, true>(h, g, 1);
 }
 
 // ---------------------------------------------------------------------------------------
+// Householder factors of a blocked QR of an m x n matrix: explicit Y (m x n, ld ldy) and
+// its transpose Yt (n x m, ld ldyt), T blocks in h->Tb.  Y(i0:, i0:i0+nb) is panel i0.
+// ---------------------------------------------------------------------------------------
+struct Fac {
+  double* Y; long long ldy;
+  double* Yt; long long ldyt;
+  const double* Yp(int i0) const { return Y + i0 + (long long)i0 * ldy; }
+  const double* Ytp(int i0) const { return Yt + i0 + (long long)i0 * ldyt; }
+};
+
+// ---------------------------------------------------------------------------------------
 // compact-WY application:  C (m x ncols) <- (I - Y op(T) Y^T) C,
 //   trans = 1: op(T) = T^T  (H_{nb-1}..H_0 C, i.e. Q^T C)
 //   trans = 0: op(T) = T    (H_0..H_{nb-1} C, i.e. Q C)
-// W0 = Y^T C (split-K DMMA GEMM) -> W = op(T) W0 (k_wy_reduce) -> C -= Y W (DMMA GEMM)
+// W0 = Y^T C (split-K TN GEMM) -> W = op(T) W0 (k_wy_reduce) -> C -= (Y^T)^T W (TN GEMM)
 // ---------------------------------------------------------------------------------------
 int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long long ldy,
-             const double* T, int nb, double* C, long long ldc) {
+             const double* Yt, long long ldyt, const double* T, int nb, double* C, long long ldc) {
   if (m <= 0 || ncols <= 0) return 0;
-  const int tilesN = cdiv(ncols, TileM::BN);
+  const int tilesN = cdiv(ncols, 128);
   int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesN), std::max(1, m / 256)));
   int kchunk = cdiv(cdiv(m, splits), 16) * 16;
   splits = cdiv(m, kchunk);
@@ -221,23 +339,28 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
     set_err("wy_apply: split-K workspace too small");
     return SDC_ERR_CUDA;
   }
-  GemmArgs g{nb, ncols, m, Y, ldy, C, ldc, h->Wp, nb, 1.0, 0.0, nullptr, 0, 0.0, kchunk,
-             (long long)nb * ncols};
-  SDC_TRY((launch_gemm_tile<true, false>(h, g, splits)));
+  h->gemm_sub = SDC_PROF_GEMM_W0;
+  int rc0 = gemm_tn(h, nb, ncols, m, 1.0, Y, ldy, C, ldc, 0.0, h->Wp, nb, nullptr, 0, 0.0, splits,
+                    kchunk, (long long)nb * ncols);
+  h->gemm_sub = SDC_PROF_GEMM_OTHER;
+  SDC_TRY(rc0);
   {
     ProfScope ps(h, SDC_PROF_WYRED, 8.0 * ((double)splits * nb * ncols + (double)nb * ncols));
     k_wy_reduce<<<cdiv(ncols, WYR_COLS), 256, 0, h->st>>>(h->Wp, splits, (long long)nb * ncols, nb,
                                                           ncols, T, trans, h->W);
     SDC_LAUNCHED(h);
   }
-  return gemm(h, false, false, m, ncols, nb, -1.0, Y, ldy, h->W, nb, 1.0, C, ldc);
+  h->gemm_sub = SDC_PROF_GEMM_UPD;
+  int rc1 = gemm_tn(h, m, ncols, nb, -1.0, Yt, ldyt, h->W, nb, 1.0, C, ldc);
+  h->gemm_sub = SDC_PROF_GEMM_OTHER;
+  return rc1;
 }
 
 // ---------------------------------------------------------------------------------------
 // panel (cooperative) and blocked QR
 // ---------------------------------------------------------------------------------------
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
-          double* T, double* tau) {
+          double* Yt, long long ldyt, double* T, double* tau) {
   int G = std::min(h->num_sms, std::max(1, m / 128));
   int rows_per = cdiv(m, G);
   if (rows_per < nb) {
@@ -256,9 +379,10 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     }
     attr_smem = smem;
   }
-  PanelArgs a{P, ldp, m, nb, Y, ldy, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count, rows_per};
+  PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
+              rows_per};
   void* args[] = {&a};
-  ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 3.0 * m * nb);   // read panel, write panel + Y
+  ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(G), dim3(PANEL_THREADS),
                                      args, smem, h->st));
   h->launches++;
@@ -268,51 +392,48 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
 
 inline double* Tblk(sdc_handle* h, int i0) { return h->Tb + (size_t)(i0 / NB) * NB * NB; }
 
-// A (m x n, m >= n) <- Householder QR in place; Y (m x n, explicit) and T blocks out.
-int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, double* Y, long long ldy) {
+// A (m x n, m >= n) <- Householder QR in place; factors into f, T blocks into h->Tb.
+int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
   for (int i0 = 0; i0 < n; i0 += NB) {
     int nbp = std::min(NB, n - i0);
-    double* Yp = Y + i0 + (long long)i0 * ldy;
-    SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, Yp, ldy, Tblk(h, i0),
-                  h->tau + i0));
+    SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, f.Y + i0 + (long long)i0 * f.ldy,
+                  f.ldy, f.Yt + i0 + (long long)i0 * f.ldyt, f.ldyt, Tblk(h, i0), h->tau + i0));
     if (i0 + nbp < n)
-      SDC_TRY(wy_apply(h, 1, m - i0, n - i0 - nbp, Yp, ldy, Tblk(h, i0), nbp,
-                       A + i0 + (long long)(i0 + nbp) * lda, lda));
+      SDC_TRY(wy_apply(h, 1, m - i0, n - i0 - nbp, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0),
+                       nbp, A + i0 + (long long)(i0 + nbp) * lda, lda));
   }
   return 0;
 }
 
 // C (m x ncols) <- Q^T C  (forward over panels) for the last blocked_qr of an m x n matrix
-int apply_qt(sdc_handle* h, int m, int n, const double* Y, long long ldy, double* C, long long ldc,
-             int ncols) {
+int apply_qt(sdc_handle* h, int m, int n, const Fac& f, double* C, long long ldc, int ncols) {
   for (int i0 = 0; i0 < n; i0 += NB) {
     int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 1, m - i0, ncols, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+    SDC_TRY(wy_apply(h, 1, m - i0, ncols, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
                      C + i0, ldc));
   }
   return 0;
 }
 
 // C (m x ncols) <- Q C  (backward over panels)
-int apply_q(sdc_handle* h, int m, int n, const double* Y, long long ldy, double* C, long long ldc,
-            int ncols) {
+int apply_q(sdc_handle* h, int m, int n, const Fac& f, double* C, long long ldc, int ncols) {
   int last = ((n - 1) / NB) * NB;
   for (int i0 = last; i0 >= 0; i0 -= NB) {
     int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 0, m - i0, ncols, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+    SDC_TRY(wy_apply(h, 0, m - i0, ncols, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
                      C + i0, ldc));
   }
   return 0;
 }
 
 // explicit square Q (n x n) = H_0..H_{n-1} (dorgqr order: only the trailing block changes)
-int form_q(sdc_handle* h, int n, const double* Y, long long ldy, double* Q, long long ldq) {
+int form_q(sdc_handle* h, int n, const Fac& f, double* Q, long long ldq) {
   k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Q, ldq, n, n, 1.0);
   SDC_LAUNCHED(h);
   int last = ((n - 1) / NB) * NB;
   for (int i0 = last; i0 >= 0; i0 -= NB) {
     int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 0, n - i0, n - i0, Y + i0 + (long long)i0 * ldy, ldy, Tblk(h, i0), nbp,
+    SDC_TRY(wy_apply(h, 0, n - i0, n - i0, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
                      Q + i0 + (long long)i0 * ldq, ldq));
   }
   return 0;
@@ -334,6 +455,9 @@ int norms(sdc_handle* h, const double* X, long long ldx, int n, double* out2) {
   return 0;
 }
 
+Fac fac_stack(sdc_handle* h, int n) { return Fac{h->Y, 2LL * n, h->Yt, (long long)n}; }
+Fac fac_square(sdc_handle* h, int n) { return Fac{h->Y, (long long)n, h->Yt, (long long)n}; }
+
 // ---------------------------------------------------------------------------------------
 // one IRS pass: S holds [B_j; -A_j]; writes A_{j+1}, B_{j+1} and the next stack into S
 // ---------------------------------------------------------------------------------------
@@ -341,7 +465,8 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
              long long ldb, double* An, long long ldan, double* Bn, long long ldbn, double* S,
              int rtest_slot, double* Rout, long long ldr) {
   const long long m = 2LL * n;
-  SDC_TRY(blocked_qr(h, S, m, (int)m, n, h->Y, m));
+  const Fac f = fac_stack(h, n);
+  SDC_TRY(blocked_qr(h, S, m, (int)m, n, f));
   if (rtest_slot >= 0) {
     k_rtest_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(S, m, h->Rprev, n, h->vec,
                                                                   h->vec + h->n_max);
@@ -361,48 +486,53 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
   // complement [Q12; Q22] = H_0..H_{n-1} [0; I]
   k_set_zero_identity<<<ew_grid(m * n), 256, 0, h->st>>>(h->C, m, n);
   SDC_LAUNCHED(h);
-  SDC_TRY(apply_q(h, (int)m, n, h->Y, m, h->C, m, n));
+  SDC_TRY(apply_q(h, (int)m, n, f, h->C, m, n));
   // A_{j+1} = Q12^T A_j (-> next stack lower half, negated); B_{j+1} = Q22^T B_j (upper)
-  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, h->C, m, Aj, lda, 0.0, An, ldan, S + n, m, -1.0));
-  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, h->C + n, m, Bj, ldb, 0.0, Bn, ldbn, S, m, 1.0));
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C, m, Aj, lda, 0.0, An, ldan, S + n, m, -1.0));
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C + n, m, Bj, ldb, 0.0, Bn, ldbn, S, m, 1.0));
   return 0;
 }
 
 // Q = GRURV(2, A_p+B_p, A_p; -1, +1)   (Alg. 2 with Alg. 1)
-int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* V,
-                long long ldv, double* Q, long long ldq) {
+// Vt = V^T (prepared once per split).
+int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* Vt,
+                double* Q, long long ldq) {
   const long long ld = n;
+  const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
   SDC_LAUNCHED(h);                                                     // S = A_p + B_p
-  SDC_TRY(gemm(h, false, true, n, n, n, 1.0, Ap, ld, V, ldv, 0.0, h->G2, ld));  // X = A_p V^T
-  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, h->Y, ld));                   // X = U R_2
-  SDC_TRY(apply_qt(h, n, n, h->Y, ld, h->G1, ld, n));                  // U^T S
+  SDC_TRY(transpose_rev(h, h->G3, ld, Ap, ld, n, 0));                  // A_p^T
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->G3, ld, Vt, ld, 0.0, h->G2, ld)); // X = A_p V^T
+  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, f));                          // X = U R_2
+  SDC_TRY(apply_qt(h, n, n, f, h->G1, ld, n));                         // U^T S
   k_row_sign<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, h->G2, ld, n, n);
   SDC_LAUNCHED(h);                                                     // U <- U D_U
   SDC_TRY(transpose_rev(h, h->G3, ld, h->G1, ld, n, 1));               // M = C^T J
-  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, h->Y, ld));                   // M = Q_qr R_qr
-  SDC_TRY(form_q(h, n, h->Y, ld, h->G1, ld));                          // Q_qr explicit
+  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, f));                          // M = Q_qr R_qr
+  SDC_TRY(form_q(h, n, f, h->G1, ld));                                 // Q_qr explicit
   k_col_sign_rev<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Q, ldq, h->G1, ld, h->G3, ld, n, 1);
   SDC_LAUNCHED(h);                                                     // Q = Q_qr D J
   return 0;
 }
 
-// Q_L = GRURV(2, A'_p^T, (A'_p+B'_p)^T; +1, -1)  (Alg. 4 line 4)
-int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* VL,
-               long long ldv, double* QL, long long ldq) {
+// Q_L = GRURV(2, A'_p^T, (A'_p+B'_p)^T; +1, -1)  (Alg. 4 line 4); VLt = V_L^T
+int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* VLt,
+               double* QL, long long ldq) {
   const long long ld = n;
+  const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
   SDC_LAUNCHED(h);
-  SDC_TRY(gemm(h, false, true, n, n, n, 1.0, h->G1, ld, VL, ldv, 0.0, h->G2, ld));  // X'
+  SDC_TRY(transpose_rev(h, h->G3, ld, h->G1, ld, n, 0));               // (A'+B')^T
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->G3, ld, VLt, ld, 0.0, h->G2, ld)); // X' = (A'+B') V_L^T
   SDC_TRY(transpose_rev(h, h->G3, ld, h->G2, ld, n, 2));               // J X' J
-  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, h->Y, ld));                   // = Qt Rt  (QL of X')
+  SDC_TRY(blocked_qr(h, h->G3, ld, n, n, f));                          // = Qt Rt  (QL of X')
   SDC_TRY(transpose_rev(h, h->G1, ld, Ap, ld, n, 3));                  // J A'_p
-  SDC_TRY(apply_qt(h, n, n, h->Y, ld, h->G1, ld, n));                  // Qt^T J A'_p
+  SDC_TRY(apply_qt(h, n, n, f, h->G1, ld, n));                         // Qt^T J A'_p
   k_row_sign<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, h->G3, ld, n, n);
   SDC_LAUNCHED(h);                                                     // D Qt^T J A'_p
   SDC_TRY(transpose_rev(h, h->G2, ld, h->G1, ld, n, 1));               // Z = A'^T U
-  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, h->Y, ld));
-  SDC_TRY(form_q(h, n, h->Y, ld, h->G1, ld));
+  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, f));
+  SDC_TRY(form_q(h, n, f, h->G1, ld));
   k_col_sign_rev<<<ew_grid((long long)n * n), 256, 0, h->st>>>(QL, ldq, h->G1, ld, h->G2, ld, n, 0);
   SDC_LAUNCHED(h);
   return 0;
@@ -427,16 +557,16 @@ int select_dev(sdc_handle* h, int n, const double* Ah, long long ldah, const dou
   return 0;
 }
 
-// Ahat = QL^T A Q (+ Bhat), split selection -> scal[4..6]
+// Ahat = QL^T A Q = (A^T QL)^T Q (+ Bhat), split selection -> scal[4..6]
 int similarity_select(sdc_handle* h, int n, const double* A, long long lda, const double* B,
                       long long ldb, const double* Q, long long ldq, const double* QL,
                       long long ldql) {
   const long long ld = n;
-  SDC_TRY(gemm(h, false, false, n, n, n, 1.0, A, lda, Q, ldq, 0.0, h->T1, ld));
-  SDC_TRY(gemm(h, true, false, n, n, n, 1.0, QL, ldql, h->T1, ld, 0.0, h->Ah, ld));
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, A, lda, QL, ldql, 0.0, h->T1, ld));     // G = A^T QL
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->T1, ld, Q, ldq, 0.0, h->Ah, ld));    // G^T Q
   if (B) {
-    SDC_TRY(gemm(h, false, false, n, n, n, 1.0, B, ldb, Q, ldq, 0.0, h->T1, ld));
-    SDC_TRY(gemm(h, true, false, n, n, n, 1.0, QL, ldql, h->T1, ld, 0.0, h->Bh, ld));
+    SDC_TRY(gemm_tn(h, n, n, n, 1.0, B, ldb, QL, ldql, 0.0, h->T1, ld));
+    SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->T1, ld, Q, ldq, 0.0, h->Bh, ld));
   }
   SDC_TRY(select_dev(h, n, h->Ah, ld, B ? h->Bh : nullptr, ld, h->scal, h->scal + 2, h->scal + 4));
   k_e21_fro_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(h->Ah, ld, n, h->scal + 4, h->vec);
@@ -542,6 +672,8 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc) rc = dalloc(h, &(p), (e))
   ALLOC(h->S, 2 * nn);
   ALLOC(h->Y, 2 * nn);
+  ALLOC(h->Yt, 2 * nn);
+  ALLOC(h->Vt, nn);
   ALLOC(h->C, 2 * nn);
   ALLOC(h->A[0], nn); ALLOC(h->A[1], nn); ALLOC(h->B[0], nn); ALLOC(h->B[1], nn);
   ALLOC(h->G1, nn); ALLOC(h->G2, nn); ALLOC(h->G3, nn); ALLOC(h->T1, nn); ALLOC(h->Ah, nn);
@@ -549,7 +681,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (h->pencil) {
     ALLOC(h->SL, 2 * nn);
     ALLOC(h->AL[0], nn); ALLOC(h->AL[1], nn); ALLOC(h->BL[0], nn); ALLOC(h->BL[1], nn);
-    ALLOC(h->Bh, nn); ALLOC(h->QLb, nn);
+    ALLOC(h->Bh, nn); ALLOC(h->QLb, nn); ALLOC(h->VLt, nn);
   }
   ALLOC(h->Tb, (n / NB + 1) * NB * NB);
   ALLOC(h->tau, n + NB);
@@ -621,6 +753,8 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
     k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->SL, m, h->AL[0], ld, h->BL[0], ld, n);
     SDC_LAUNCHED(h);
   }
+  SDC_TRY(transpose_rev(h, h->Vt, ld, V, ldv, n, 0));                   // V^T (K-major operand)
+  if (pencil) SDC_TRY(transpose_rev(h, h->VLt, ld, VL, ldvl, n, 0));
   double* QLd = pencil ? h->QLb : nullptr;
   std::vector<double> hbuf;
   if (hist_cap > 0) hbuf.assign((size_t)hist_cap * 3, NAN);
@@ -642,8 +776,8 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
       if (ratio <= tol) { p = j + 1; conv = 1; break; }
     }
     if (stop_mode == SDC_STOP_E21) {
-      SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], V, ldv, Q, ldq));
-      if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], VL, ldvl, QLd, ld));
+      SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
+      if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
       SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
       have_split = true;
       SDC_CK(cudaMemcpyAsync(hsel, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
@@ -653,8 +787,8 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
     }
   }
   if (!have_split) {
-    SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], V, ldv, Q, ldq));
-    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], VL, ldvl, QLd, ld));
+    SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
+    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
     SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
   }
   SDC_CK(cudaMemsetAsync(h->flag, 0, sizeof(int), h->st));
@@ -723,7 +857,7 @@ int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N,
   if (ldb < std::max(1, transb ? N : K)) { set_err("invalid argument (ldb < std::max(1, transb ? N : K))"); return -12; }
   if (ldc < std::max(1, M)) { set_err("invalid argument (ldc < std::max(1, M))"); return -15; }
   h->st = static_cast<cudaStream_t>(stream);
-  return gemm(h, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  return gemm_general(h, transa != 0, transb != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double* Qthin, int ldq) {
@@ -735,11 +869,12 @@ int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double
   h->st = static_cast<cudaStream_t>(stream);
   SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
   h->bar_count = 0;
-  SDC_TRY(blocked_qr(h, A, lda, m, n, h->Y, m));
+  const Fac f{h->Y, (long long)m, h->Yt, (long long)n};
+  SDC_TRY(blocked_qr(h, A, lda, m, n, f));
   if (Qthin) {
     k_set_identity<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, 1.0);
     SDC_LAUNCHED(h);
-    SDC_TRY(apply_q(h, m, n, h->Y, m, Qthin, ldq, n));
+    SDC_TRY(apply_q(h, m, n, f, Qthin, ldq, n));
     k_col_sign<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, A, lda);
     SDC_LAUNCHED(h);
   }
