@@ -146,6 +146,12 @@ enum { SDC_PROF_GEMM = 0,        /* every DMMA GEMM launch                      
 int sdc_profile(sdc_handle* h, int enable);
 int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, double* work);
 
+/* Debug counters (enabled by env SDC_DEBUG_COUNTERS at sdc_create): copies `count` (<= 64)
+ * device counters to the HOST array `out`; reset != 0 zeroes them.  Slots 0-3 / 4-7: panel
+ * kernel clock64 cycles (partials, grid barrier, partial sums, update) of CTA 0 / the last
+ * CTA summed over columns; slot 8: number of timed panel CTAs. */
+int sdc_debug_counters(sdc_handle* h, unsigned long long* out, int count, int reset);
+
 /* Number of kernels launched by this handle since creation (evidence counter). */
 long long sdc_kernel_launches(const sdc_handle* h);
 

@@ -35,6 +35,7 @@ _SIGS = {
     "sdc_split_select": (I, [P, P, I, P, I, D, P, I, D, ctypes.POINTER(I), ctypes.POINTER(D), P]),
     "sdc_kernel_launches": (LL, [P]),
     "sdc_profile": (I, [P, I]),
+    "sdc_debug_counters": (I, [P, P, I, I]),
     "sdc_profile_read": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(LL), ctypes.POINTER(D)]),
     "sdc_last_error": (ctypes.c_char_p, []),
 }

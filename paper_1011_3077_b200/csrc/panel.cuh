@@ -13,11 +13,13 @@
 // Per column k ONE grid-wide reduction of nb numbers suffices:
 //   part[j] = sum_{rows r > k} x_r P[r][j],  x = P[:,k]
 // gives sigma = ||x_below||^2 (j = k), the update inner products z_j (j > k) and the
-// Gram entries Y(:,i)^T x (i < k) that build the compact-WY T column:
+// Gram entries x_i^T x (i < k) that build the compact-WY T column:
 //   w_j   = tau (P[k][j] + scale z_j),           P[r][j] -= w_j * scale * x_r
-//   g_i   = Y[k][i] + scale * part[i],           T(0:k,k) = -tau T(0:k,0:k) g, T(k,k)=tau
-// Each CTA sums the per-CTA partials in the same fixed order, so all CTAs agree
-// bit-for-bit and the result is run-to-run deterministic.
+//   g_i   = s_i (x_i[k] + scale * part[i]),      T(0:k,k) = -tau T(0:k,0:k) g, T(k,k)=tau
+// Reflector columns stay unscaled in shared memory (v_i = s_i x_i, applied at write-back),
+// so no thread ever reads a column another thread is rewriting in the same step: 3 CTA
+// barriers + 1 grid barrier per column.  Each CTA sums the per-CTA partials in the same
+// fixed order, so all CTAs agree bit-for-bit and the result is run-to-run deterministic.
 #pragma once
 #include "common.cuh"
 
@@ -38,7 +40,26 @@ struct PanelArgs {
   unsigned int* bar;          // grid barrier counter
   unsigned int bar_base;      // value of *bar before this launch (sum of G*nb of earlier launches)
   int rows_per;               // rows owned per CTA (CTA 0 owns rows [0, rows_per) >= nb)
+  unsigned long long* dbg;    // optional phase timers (CTA 0 / last CTA, thread 0), or null
 };
+
+// T column c of the compact-WY factor (CTA 0), from the step-c reduction results:
+//   g_i = s_i (x_i[c] + scale_c * sum_{r>c} x_i[r] x_c[r])  = Y(:,i)^T v_c   (i < c)
+//   T(0:c, c) = -tau_c T(0:c, 0:c) g,  T(c, c) = tau_c
+// (columns are kept unscaled in shared memory; s_i is the scale that turns x_i into v_i)
+SDC_DEV void panel_t_column(double* Ts, int c, const double* tot, const double* drow,
+                            const double* sc, const double* tauv) {
+  const int i = threadIdx.x >> 2, q = threadIdx.x & 3;
+  const double tau = tauv[c], scale = sc[c];
+  double acc = 0.0;
+  if (i < c)
+    for (int l = i + q; l < c; l += 4)
+      acc = fma(Ts[l * PANEL_NB + i], sc[l] * fma(scale, tot[l], drow[l]), acc);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  if (i < c && q == 0) Ts[c * PANEL_NB + i] = -tau * acc;
+  if (threadIdx.x == 0) Ts[c * PANEL_NB + c] = tau;
+}
 
 __global__ void __launch_bounds__(PANEL_THREADS)
 panel_qr_kernel(const PanelArgs a) {
@@ -48,14 +69,13 @@ panel_qr_kernel(const PanelArgs a) {
   const int r0 = cta * a.rows_per;
   const int r1 = min(a.m, r0 + a.rows_per);
   const int R = max(0, r1 - r0);
-  double* Ps = sm;                                  // R x PANEL_LD
-  double* xs = Ps + (size_t)a.rows_per * PANEL_LD;  // rows_per
-  double* red = xs + a.rows_per;                    // 4 x PANEL_NB
-  double* tot = red + 4 * PANEL_NB;                 // PANEL_NB
-  double* drow = tot + PANEL_NB;                    // PANEL_NB
-  double* Ts = drow + PANEL_NB;                     // PANEL_NB x PANEL_NB (CTA 0), col-major
-  double* wv = Ts + PANEL_NB * PANEL_NB;            // PANEL_NB
-  __shared__ double s_tau, s_scale, s_beta;
+  double* Ps = sm;                                  // R x PANEL_LD, row-major local block
+  double* red = Ps + (size_t)a.rows_per * PANEL_LD; // 4 x PANEL_NB
+  double* totb = red + 4 * PANEL_NB;                // 2 x PANEL_NB (by column parity)
+  double* drowb = totb + 2 * PANEL_NB;              // 2 x PANEL_NB
+  double* sc = drowb + 2 * PANEL_NB;                // PANEL_NB: v_i = sc[i] * x_i
+  double* tauv = sc + PANEL_NB;                     // PANEL_NB
+  double* Ts = tauv + PANEL_NB;                     // PANEL_NB x PANEL_NB (CTA 0), col-major
 
   // load the CTA's row block
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {
@@ -67,24 +87,27 @@ panel_qr_kernel(const PanelArgs a) {
   __syncthreads();
 
   const int jj = tid & (PANEL_NB - 1), rg = tid >> 6;  // column lane, row group (0..3)
+  const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
+  unsigned long long ph[4] = {0, 0, 0, 0}, t0 = 0, t1;
   for (int k = 0; k < nb; ++k) {
-    // rows r (local) with global index > k
-    const int lbeg = max(0, k + 1 - r0);
-    for (int r = lbeg + tid; r < R; r += PANEL_THREADS) xs[r] = Ps[r * PANEL_LD + k];
-    __syncthreads();
-    // partial dot products part[j] = sum_r x_r P[r][j]
+    if (timed) t0 = clock64();
+    const int lbeg = max(0, k + 1 - r0);               // local rows with global index > k
+    // (a) partial inner products part[j] = sum_{r > k} x_r P[r][j], x = P[:,k]
     double s = 0.0;
     if (jj < nb) {
       double s1 = 0.0;
       int r = lbeg + rg;
       for (; r + 4 < R; r += 8) {
-        s = fma(xs[r], Ps[r * PANEL_LD + jj], s);
-        s1 = fma(xs[r + 4], Ps[(r + 4) * PANEL_LD + jj], s1);
+        s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
+        s1 = fma(Ps[(r + 4) * PANEL_LD + k], Ps[(r + 4) * PANEL_LD + jj], s1);
       }
-      if (r < R) s = fma(xs[r], Ps[r * PANEL_LD + jj], s);
+      if (r < R) s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
       s += s1;
     }
     red[rg * PANEL_NB + jj] = s;
+    if (cta == 0 && k > 0)   // T column of the previous step (its inputs are double-buffered)
+      panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
+                     sc, tauv);
     __syncthreads();
     double* gb = a.gbuf + (size_t)(k & 1) * (G + 1) * PANEL_NB;
     if (tid < nb) {
@@ -92,13 +115,22 @@ panel_qr_kernel(const PanelArgs a) {
       __stcg(gb + (size_t)cta * PANEL_NB + tid, p);
       if (cta == 0) __stcg(gb + (size_t)G * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);  // row k
     }
+    if (timed) { t1 = clock64(); ph[0] += t1 - t0; t0 = t1; }
     grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
-    // all CTAs: fixed-order sum over CTAs
+    if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
+    // (b) every CTA sums the per-CTA partials in the same fixed order
     {
       double t = 0.0;
       if (jj < nb) {
         int c = rg;
-        for (; c + 28 < G; c += 32) {   // batch 8 independent L2 loads, add in order
+        for (; c + 60 < G; c += 64) {   // batch 16 independent L2 loads, add in order
+          double v[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = __ldcg(gb + (size_t)(c + 4 * u) * PANEL_NB + jj);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) t += v[u];
+        }
+        for (; c + 28 < G; c += 32) {
           double v[8];
 #pragma unroll
           for (int u = 0; u < 8; ++u) v[u] = __ldcg(gb + (size_t)(c + 4 * u) * PANEL_NB + jj);
@@ -110,61 +142,64 @@ panel_qr_kernel(const PanelArgs a) {
       red[rg * PANEL_NB + jj] = t;
     }
     __syncthreads();
-    if (tid < nb) {
-      tot[tid] = ((red[tid] + red[PANEL_NB + tid]) + red[2 * PANEL_NB + tid]) + red[3 * PANEL_NB + tid];
-      drow[tid] = __ldcg(gb + (size_t)G * PANEL_NB + tid);
+    if (timed) { t1 = clock64(); ph[2] += t1 - t0; t0 = t1; }
+    // (c) reflector of column k, computed redundantly by every thread (identical values)
+    const double alpha = __ldcg(gb + (size_t)G * PANEL_NB + k);
+    const double sigma = ((red[k] + red[PANEL_NB + k]) + red[2 * PANEL_NB + k]) + red[3 * PANEL_NB + k];
+    double tau = 0.0, scale = 0.0, beta = alpha;
+    if (sigma != 0.0) {
+      const double nrm = sqrt(alpha * alpha + sigma);
+      beta = alpha < 0.0 ? nrm : -nrm;
+      tau = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
     }
-    __syncthreads();
+    if (jj < nb) {
+      const double totj = ((red[jj] + red[PANEL_NB + jj]) + red[2 * PANEL_NB + jj]) + red[3 * PANEL_NB + jj];
+      const double drowj = __ldcg(gb + (size_t)G * PANEL_NB + jj);
+      if (rg == 0) { totb[(k & 1) * PANEL_NB + jj] = totj; drowb[(k & 1) * PANEL_NB + jj] = drowj; }
+      if (jj > k) {
+        // H_k applied to column jj: w = tau (P[k][jj] + scale z_jj); rows r > k: P -= w scale x_r
+        const double w = tau * fma(scale, totj, drowj);
+        const double ws = w * scale;
+#pragma unroll 4
+        for (int r = lbeg + rg; r < R; r += 4)
+          Ps[r * PANEL_LD + jj] = fma(-ws, Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj]);
+        if (cta == 0 && rg == 0) Ps[k * PANEL_LD + jj] -= w;      // diagonal row k
+      }
+    }
     if (tid == 0) {
-      double alpha = drow[k], sigma = tot[k];
-      double tau = 0.0, scale = 0.0, beta = alpha;
-      if (sigma != 0.0) {
-        double nrm = sqrt(alpha * alpha + sigma);
-        beta = alpha < 0.0 ? nrm : -nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      s_tau = tau; s_scale = scale; s_beta = beta;
+      sc[k] = scale;
+      tauv[k] = tau;
+      if (cta == 0) { Ps[k * PANEL_LD + k] = beta; a.tau[k] = tau; }
     }
     __syncthreads();
-    const double tau = s_tau, scale = s_scale;
-    if (tid < nb) wv[tid] = (tid > k) ? tau * fma(scale, tot[tid], drow[tid]) : 0.0;
-    __syncthreads();
-    // update local rows below the diagonal, turn column k into v
-    for (int e = tid; e < (R - lbeg) * nb; e += PANEL_THREADS) {
-      int r = lbeg + e / nb, j = e % nb;
-      double xv = xs[r] * scale;
-      if (j > k) Ps[r * PANEL_LD + j] = fma(-wv[j], xv, Ps[r * PANEL_LD + j]);
-      else if (j == k) Ps[r * PANEL_LD + j] = xv;
-    }
-    if (cta == 0) {
-      if (tid < nb && tid > k) Ps[k * PANEL_LD + tid] -= wv[tid];
-      if (tid == 0) { Ps[k * PANEL_LD + k] = s_beta; a.tau[k] = tau; }
-      // T column k:  g_i = Y[k][i] + scale * part[i] (i < k);  T(0:k,k) = -tau T g
-      if (tid < k) {
-        double acc = 0.0;
-        for (int l = tid; l < k; ++l)
-          acc = fma(Ts[l * PANEL_NB + tid], fma(scale, tot[l], drow[l]), acc);
-        Ts[k * PANEL_NB + tid] = -tau * acc;
-      }
-      if (tid == k) Ts[k * PANEL_NB + k] = tau;
-    }
-    __syncthreads();
+    if (timed) { t1 = clock64(); ph[3] += t1 - t0; }
+  }
+  if (cta == 0) {
+    panel_t_column(Ts, nb - 1, totb + ((nb - 1) & 1) * PANEL_NB, drowb + ((nb - 1) & 1) * PANEL_NB,
+                   sc, tauv);
+  }
+  __syncthreads();
+  if (timed) {
+    const int o = cta == 0 ? 0 : 4;
+    for (int q = 0; q < 4; ++q) atomicAdd(a.dbg + o + q, ph[q]);
+    atomicAdd(a.dbg + 8, 1ull);
   }
 
-  // write back: factored panel (R above / v below) and explicit Y
+  // write back: R above the diagonal, v = s_j x below it (LAPACK layout), explicit Y, Y^T
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {
     int j = e / R, r = e % R;
     int gr = r0 + r;
-    double v = Ps[r * PANEL_LD + j];
+    double x = Ps[r * PANEL_LD + j];
+    double v = gr > j ? sc[j] * x : x;
     a.P[(long long)gr + (long long)j * a.ldp] = v;
     a.Y[(long long)gr + (long long)j * a.ldy] = gr > j ? v : (gr == j ? 1.0 : 0.0);
   }
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {     // Y^T: contiguous along j
     int r = e / nb, j = e % nb;
     int gr = r0 + r;
-    double v = Ps[r * PANEL_LD + j];
-    a.Yt[(long long)j + (long long)gr * a.ldyt] = gr > j ? v : (gr == j ? 1.0 : 0.0);
+    double v = gr > j ? sc[j] * Ps[r * PANEL_LD + j] : (gr == j ? 1.0 : 0.0);
+    a.Yt[(long long)j + (long long)gr * a.ldyt] = v;
   }
   if (cta == 0)
     for (int e = tid; e < nb * nb; e += PANEL_THREADS) {
@@ -174,8 +209,8 @@ panel_qr_kernel(const PanelArgs a) {
 }
 
 inline size_t panel_smem_bytes(int rows_per) {
-  return sizeof(double) * ((size_t)rows_per * PANEL_LD + rows_per + 4 * PANEL_NB + 2 * PANEL_NB +
-                           PANEL_NB * PANEL_NB + PANEL_NB);
+  return sizeof(double) * ((size_t)rows_per * PANEL_LD + 4 * PANEL_NB + 4 * PANEL_NB + 2 * PANEL_NB +
+                           PANEL_NB * PANEL_NB);
 }
 
 }  // namespace sdc

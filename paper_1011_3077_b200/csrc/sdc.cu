@@ -79,6 +79,9 @@ struct sdc_handle {
   unsigned long long bar_count = 0;
   int* flag = nullptr;
   long long launches = 0;
+  unsigned long long* dbg = nullptr;   // debug counters (sdc_debug_counters)
+  bool dbg_on = false;
+  int panel_rows = 128;                // target rows per panel CTA
   // optional per-kernel-class timing with CUDA events on the launching stream
   bool prof_on = false;
   int gemm_sub = SDC_PROF_GEMM_OTHER;   // sub-class of the GEMMs being launched
@@ -361,7 +364,7 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
 // ---------------------------------------------------------------------------------------
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau) {
-  int G = std::min(h->num_sms, std::max(1, m / 128));
+  int G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
   int rows_per = cdiv(m, G);
   if (rows_per < nb) {
     rows_per = nb;
@@ -380,7 +383,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     attr_smem = smem;
   }
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
-              rows_per};
+              rows_per, h->dbg_on ? h->dbg : nullptr};
   void* args[] = {&a};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(G), dim3(PANEL_THREADS),
@@ -616,6 +619,14 @@ const char* sdc_last_error(void) { return g_err; }
 
 long long sdc_kernel_launches(const sdc_handle* h) { return h ? h->launches : 0; }
 
+int sdc_debug_counters(sdc_handle* h, unsigned long long* out, int count, int reset) {
+  if (!h || count < 0 || count > 64) return -1;
+  if (count && cudaMemcpy(out, h->dbg, sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return SDC_ERR_CUDA;
+  if (reset) cudaMemset(h->dbg, 0, 64 * sizeof(unsigned long long));
+  return 0;
+}
+
 int sdc_profile(sdc_handle* h, int enable) {
   if (!h) return -1;
   prof_collect(h);
@@ -700,6 +711,13 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     if (e != cudaSuccess) { set_err("cudaMalloc: %s", cudaGetErrorString(e)); rc = SDC_ERR_NOMEM; }
     else { h->allocs.push_back(q); h->bar = (unsigned*)q; h->flag = (int*)((char*)q + 32); }
   }
+  if (!rc) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, 64 * sizeof(unsigned long long)) != cudaSuccess) rc = SDC_ERR_NOMEM;
+    else { h->allocs.push_back(q); h->dbg = (unsigned long long*)q; cudaMemset(q, 0, 64 * 8); }
+  }
+  if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
+  if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
   if (rc) { sdc_destroy(h); return rc; }
   *out = h;
   return 0;
