@@ -23,6 +23,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -99,29 +101,36 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # CPU oracle: a bounded sample, extrapolated by the flop model
 # ---------------------------------------------------------------------------------------
-def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 768):
-    """Time the plain oracle (as it stands) on a same-recipe sample at n_sample:
-    1 pass (+GRURV/similarity/select) and 2 passes; per-pass = difference.  Returns the
-    extrapolated seconds of one full step at n_target (n^3 scaling of each part)."""
+def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 1536):
+    """Time the plain oracle (as it stands) on a same-recipe sample at n_sample: two IRS
+    passes (median) and one full split with a single pass; GRURV + similarity + selection
+    = split(1 pass) - pass.  Returns the extrapolated seconds of one full step at n_target
+    (each part scaled by n^3, the flop model's order), threads, description, CPU seconds."""
     import oracle
     from paper_1011_3077_b200 import inputs
     oracle.build()
     threads = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     p = inputs.make_config(4 if pencil else 5, n=n_sample)
-    t = []
-    for iters in (1, 2):
+    b0 = p.B if pencil else np.eye(n_sample)
+    oracle.irs_pass(p.A[:64, :64], b0[:64, :64])          # warm the thread pool
+    t_spent = time.perf_counter()
+    tp = []
+    for _ in range(2):
         t0 = time.perf_counter()
-        oracle.split(p.A, p.B, p.V, p.VL, max_iters=iters)
-        t.append(time.perf_counter() - t0)
-    per_pass = max(t[1] - t[0], 1e-9)
-    rest = max(t[0] - per_pass, 1e-9)
+        oracle.irs_pass(p.A, b0)
+        tp.append(time.perf_counter() - t0)
+    per_pass = statistics.median(tp) * (2 if pencil else 1)
+    t0 = time.perf_counter()
+    oracle.split(p.A, p.B, p.V, p.VL, max_iters=1)
+    t1 = time.perf_counter() - t0
+    rest = max(t1 - per_pass, 1e-9)
     scale = (n_target / n_sample) ** 3
     total = (passes * per_pass + rest) * scale
-    sample = (f"oracle.split at n={n_sample} (same recipe) with 1 and 2 passes: "
-              f"{per_pass:.2f} s/pass, {rest:.2f} s GRURV+similarity+select; extrapolated by n^3 "
-              f"to n={n_target}, {passes} passes")
-    return total, threads, sample, sum(t)
+    sample = (f"oracle at n={n_sample} (same recipe): {per_pass:.2f} s per IRS pass (median of 2), "
+              f"{rest:.2f} s GRURV+similarity+select; extrapolated by n^3 to n={n_target}, "
+              f"{passes} passes")
+    return total, threads, sample, time.perf_counter() - t_spent
 
 
 def run_reference(args, cfg_name, n, passes, pencil, rank, world):
@@ -162,7 +171,7 @@ def main():
     ap.add_argument("--impl", default="sdc", choices=["sdc", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-n", type=int, default=768)
+    ap.add_argument("--ref-n", type=int, default=1536)
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -212,7 +221,12 @@ def main():
     st = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = h.launches
-    h.profile(True)
+    # per-kernel-class CUDA events: live inside the timed region for large n; for n small
+    # enough to run as one CUDA graph (libsdc graph_max_n = 4096) event recording would
+    # disable the graph, so the classes are timed on one extra step after the timed region
+    live_prof = n > 4096
+    if live_prof:
+        h.profile(True)
     infos = []
     with ClockSampler(local) as clk:
         barrier()
@@ -224,6 +238,11 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
     launches = (h.launches - launches0) // args.steps
+    if not live_prof:
+        h.profile(True)
+        step()
+        barrier()
+    prof_steps = args.steps if live_prof else 1
     prof = {c: h.profile_read(c) for c in range(7)}
     h.profile(False)
     if world > 1:
@@ -279,16 +298,16 @@ def main():
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
             "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak_microbench.txt)",
-            "share_of_step": (g_ms / args.steps) / ms if ms > 0 else None,
-            "launches_per_step": g_n // max(1, args.steps),
+            "share_of_step": (g_ms / prof_steps) / ms if ms > 0 else None,
+            "launches_per_step": g_n // prof_steps, "timed_live": live_prof,
             "flops_per_launch": g_flops / max(1, g_n)}
     panel = {"bound": "hbm", "kernel": "panel_qr_kernel", "achieved":
              (p_bytes / (p_ms / 1e3) / 1e9) if p_ms > 0 else None, "peak": hbm, "unit": "GB/s",
-             "peak_source": hbm_src, "share_of_step": (p_ms / args.steps) / ms if ms > 0 else None,
-             "launches_per_step": p_n // max(1, args.steps)}
+             "peak_source": hbm_src, "share_of_step": (p_ms / prof_steps) / ms if ms > 0 else None,
+             "launches_per_step": p_n // prof_steps}
     if panel["achieved"]:
         panel["frac"] = panel["achieved"] / hbm
-    others = {name: {"ms_per_step": prof[c][0] / args.steps, "launches_per_step": prof[c][1] // args.steps,
+    others = {name: {"ms_per_step": prof[c][0] / prof_steps, "launches_per_step": prof[c][1] // prof_steps,
                      "tflops": (prof[c][2] / (prof[c][0] / 1e3) / 1e12) if (c >= 4 and prof[c][0] > 0) else None}
               for c, name in ((2, "k_wy_reduce"), (3, "split_select"), (4, "gemm W0=Y^T C (split-K)"),
                               (5, "gemm rank-nb update C-=YW"), (6, "gemm n x n products"))}

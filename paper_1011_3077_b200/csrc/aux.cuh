@@ -373,4 +373,84 @@ __global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits,
   }
 }
 
+// Z = sum_z P[z] (m x n blocks, z-stride zs, ld m), fixed order
+__global__ void k_sum_partials(const double* P, int splits, long long zs, long long total, double* Z) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += P[(long long)z * zs + e];
+    Z[e] = s;
+  }
+}
+
+// Outer compact-WY block assembly.  T_O (nbo x nbo, ld nbo) and its transpose T_Ot:
+// k_tout_place zeroes both and copies the inner 64x64 T blocks onto the diagonal.
+__global__ void k_tout_place(double* TO, double* TOt, int nbo, const double* Tinner) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nbo * nbo; e += gridDim.x * blockDim.x) {
+    int i = e % nbo, j = e / nbo;
+    double v = 0.0;
+    if ((i >> 6) == (j >> 6) && i <= j) {
+      int b = i >> 6, nbb = min(64, nbo - b * 64);
+      v = Tinner[(size_t)b * 64 * 64 + (size_t)(j & 63) * nbb + (i & 63)];
+    }
+    TO[i + (long long)j * nbo] = v;
+    TOt[j + (long long)i * nbo] = v;
+  }
+}
+
+// Merge of two adjacent compact-WY blocks (the recursive T of Elmroth-Gustavson):
+//   (I - Ya Ta Ya^T)(I - Yb Tb Yb^T) = I - [Ya Yb] [[Ta, X], [0, Tb]] [Ya Yb]^T,
+//   X = -Ta (Ya^T Yb) Tb.
+// Ta = TO[a0:a0+p, a0:a0+p], Tb = TO[b0:b0+q, b0:b0+q] (upper triangular, zeros below),
+// G = Y_O^T Y_O (ld nbo).  CTA (bx, by) computes the 32x32 block of X at rows 32bx, cols
+// 32by; writes X into TO and X^T into TOt.
+__global__ void __launch_bounds__(256) k_tmerge(double* TO, double* TOt, int nbo, const double* G,
+                                                int a0, int p, int b0, int q) {
+  __shared__ double Ta[32][33];    // Ta[rb:rb+32, l0:l0+32]
+  __shared__ double Gc[32][33];    // G[a0+l0 : +32, b0+c0 : +32]
+  __shared__ double U[32][33];
+  __shared__ double Tb[32][33];
+  const int rb = blockIdx.x * 32, cb = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+  double acc[4] = {0, 0, 0, 0};
+  for (int c0 = 0; c0 < q; c0 += 32) {
+    double u[4] = {0, 0, 0, 0};
+    for (int l0 = 0; l0 < p; l0 += 32) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+        int r = e % 32, c = e / 32;
+        Ta[r][c] = (rb + r < p && l0 + c < p) ? TO[(a0 + rb + r) + (long long)(a0 + l0 + c) * nbo] : 0.0;
+        Gc[r][c] = (l0 + r < p && c0 + c < q) ? G[(a0 + l0 + r) + (long long)(b0 + c0 + c) * nbo] : 0.0;
+      }
+      __syncthreads();
+      for (int t = 0; t < 4; ++t) {      // U += Ta(32 x 32) Gc(32 x 32)
+        const int c = ty + 8 * t;
+        double sum = u[t];
+        for (int l = 0; l < 32; ++l) sum = fma(Ta[tx][l], Gc[l][c], sum);
+        u[t] = sum;
+      }
+    }
+    __syncthreads();
+    for (int t = 0; t < 4; ++t) U[tx][ty + 8 * t] = u[t];
+    for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+      int r = e % 32, c = e / 32;
+      Tb[r][c] = (c0 + r < q && cb + c < q) ? TO[(b0 + c0 + r) + (long long)(b0 + cb + c) * nbo] : 0.0;
+    }
+    __syncthreads();
+    for (int t = 0; t < 4; ++t) {        // acc += U(32 x 32) Tb(32 x 32)
+      const int c = ty + 8 * t;
+      double sum = acc[t];
+      for (int l = 0; l < 32; ++l) sum = fma(U[tx][l], Tb[l][c], sum);
+      acc[t] = sum;
+    }
+  }
+  for (int t = 0; t < 4; ++t) {
+    int r = rb + tx, c = cb + ty + 8 * t;
+    if (r < p && c < q) {
+      TO[(a0 + r) + (long long)(b0 + c) * nbo] = -acc[t];
+      TOt[(b0 + c) + (long long)(a0 + r) * nbo] = -acc[t];
+    }
+  }
+}
+
 }  // namespace sdc

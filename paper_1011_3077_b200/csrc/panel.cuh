@@ -41,6 +41,7 @@ struct PanelArgs {
   unsigned int bar_base;      // value of *bar before this launch (sum of G*nb of earlier launches)
   int rows_per;               // rows owned per CTA (CTA 0 owns rows [0, rows_per) >= nb)
   unsigned long long* dbg;    // optional phase timers (CTA 0 / last CTA, thread 0), or null
+  int zero_above;             // rows above the panel (inside its outer WY block) to zero in Y/Y^T
 };
 
 // T column c of the compact-WY factor (CTA 0), from the step-c reduction results:
@@ -201,11 +202,21 @@ panel_qr_kernel(const PanelArgs a) {
     double v = gr > j ? sc[j] * Ps[r * PANEL_LD + j] : (gr == j ? 1.0 : 0.0);
     a.Yt[(long long)j + (long long)gr * a.ldyt] = v;
   }
-  if (cta == 0)
+  if (cta == 0) {
     for (int e = tid; e < nb * nb; e += PANEL_THREADS) {
       int j = e / nb, i = e % nb;
       a.T[e] = Ts[j * PANEL_NB + i];
     }
+    // rows [-zero_above, 0) of this panel's Y columns belong to the outer block: zeros
+    for (int e = tid; e < a.zero_above * nb; e += PANEL_THREADS) {
+      int j = e / a.zero_above, r = e % a.zero_above - a.zero_above;
+      a.Y[(long long)r + (long long)j * a.ldy] = 0.0;
+    }
+    for (int e = tid; e < a.zero_above * nb; e += PANEL_THREADS) {
+      int r = e / nb - a.zero_above, j = e % nb;
+      a.Yt[(long long)j + (long long)r * a.ldyt] = 0.0;
+    }
+  }
 }
 
 inline size_t panel_smem_bytes(int rows_per) {

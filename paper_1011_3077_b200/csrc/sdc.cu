@@ -82,6 +82,28 @@ struct sdc_handle {
   unsigned long long* dbg = nullptr;   // debug counters (sdc_debug_counters)
   bool dbg_on = false;
   int panel_rows = 128;                // target rows per panel CTA
+  int nbo = 256;                       // outer compact-WY block width (multiple of 64)
+  double *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr, *Gb = nullptr;
+  // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
+  struct GraphKey {
+    int n = 0, max_iters = 0, nbo = 0;
+    const void *A = nullptr, *B = nullptr, *V = nullptr, *VL = nullptr, *Q = nullptr, *QL = nullptr,
+               *Ahat = nullptr;
+    long long lda = 0, ldb = 0, ldv = 0, ldvl = 0, ldq = 0, ldql = 0, ldah = 0;
+    bool operator==(const GraphKey& o) const {
+      return n == o.n && max_iters == o.max_iters && nbo == o.nbo && A == o.A && B == o.B && V == o.V &&
+             VL == o.VL && Q == o.Q && QL == o.QL && Ahat == o.Ahat && lda == o.lda && ldb == o.ldb &&
+             ldv == o.ldv && ldvl == o.ldvl && ldq == o.ldq && ldql == o.ldql && ldah == o.ldah;
+    }
+  } gkey;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_st = nullptr;
+  long long glaunches = 0;
+  int graph_max_n = 4096;
+  double* hscal = nullptr;             // pinned host copies of the result scalars
+  const double *cur_V = nullptr, *cur_VL = nullptr;
+  long long cur_ldv = 0, cur_ldvl = 0;
+  unsigned int* hflags = nullptr;      // pinned: [0] non-finite flag, [1] barrier error
   // optional per-kernel-class timing with CUDA events on the launching stream
   bool prof_on = false;
   int gemm_sub = SDC_PROF_GEMM_OTHER;   // sub-class of the GEMMs being launched
@@ -363,7 +385,7 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
 // panel (cooperative) and blocked QR
 // ---------------------------------------------------------------------------------------
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
-          double* Yt, long long ldyt, double* T, double* tau) {
+          double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
   int G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
   int rows_per = cdiv(m, G);
   if (rows_per < nb) {
@@ -383,7 +405,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     attr_smem = smem;
   }
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
-              rows_per, h->dbg_on ? h->dbg : nullptr};
+              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above};
   void* args[] = {&a};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(G), dim3(PANEL_THREADS),
@@ -394,37 +416,113 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
 }
 
 inline double* Tblk(sdc_handle* h, int i0) { return h->Tb + (size_t)(i0 / NB) * NB * NB; }
+inline double* TOblk(sdc_handle* h, int I0) { return h->Tob + (size_t)(I0 / h->nbo) * h->nbo * h->nbo; }
+inline double* TOtblk(sdc_handle* h, int I0) { return h->Tobt + (size_t)(I0 / h->nbo) * h->nbo * h->nbo; }
 
-// A (m x n, m >= n) <- Householder QR in place; factors into f, T blocks into h->Tb.
+// Outer compact-WY factor of the nbo columns starting at I0 (rows I0..m-1):
+// T_O from the inner 64-wide T blocks and G = Y_O^T Y_O by a merge tree.
+int build_tout(sdc_handle* h, int m, int I0, int nbo, const Fac& f) {
+  double* TO = TOblk(h, I0);
+  double* TOt = TOtblk(h, I0);
+  k_tout_place<<<cdiv((long long)nbo * nbo, 256), 256, 0, h->st>>>(TO, TOt, nbo, Tblk(h, I0));
+  SDC_LAUNCHED(h);
+  if (nbo <= NB) return 0;
+  const int rows = m - I0;
+  // G = Y_O^T Y_O (split-K TN GEMM + fixed-order sum)
+  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, cdiv(nbo, 128) * cdiv(nbo, 128)),
+                                    std::max(1, rows / 256)));
+  int kchunk = cdiv(cdiv(rows, splits), 16) * 16;
+  splits = cdiv(rows, kchunk);
+  if ((size_t)splits * nbo * nbo > h->wp_elems) { set_err("build_tout: workspace"); return SDC_ERR_CUDA; }
+  SDC_TRY(gemm_tn(h, nbo, nbo, rows, 1.0, f.Yp(I0), f.ldy, f.Yp(I0), f.ldy, 0.0, h->Wp, nbo, nullptr,
+                  0, 0.0, splits, kchunk, (long long)nbo * nbo));
+  k_sum_partials<<<cdiv((long long)nbo * nbo, 256), 256, 0, h->st>>>(h->Wp, splits, (long long)nbo * nbo,
+                                                                    (long long)nbo * nbo, h->Gb);
+  SDC_LAUNCHED(h);
+  for (int s = NB; s < nbo; s *= 2)
+    for (int a0 = 0; a0 + s < nbo; a0 += 2 * s) {
+      const int p = s, q = std::min(s, nbo - a0 - s);
+      k_tmerge<<<dim3(cdiv(p, 32), cdiv(q, 32)), 256, 0, h->st>>>(TO, TOt, nbo, h->Gb, a0, p, a0 + s, q);
+      SDC_LAUNCHED(h);
+    }
+  return 0;
+}
+
+// C (m x ncols) <- (I - Y_O op(T_O) Y_O^T) C for the outer block at I0 (rows I0.. of the
+// factored matrix = rows 0.. of C):  Z = Y_O^T C (split-K), W = op(T_O) Z, C -= Y_O W.
+int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, const Fac& f,
+                   double* C, long long ldc) {
+  if (nbo <= NB) return wy_apply(h, trans, m, ncols, f.Yp(I0), f.ldy, f.Ytp(I0), f.ldyt, Tblk(h, I0),
+                                 nbo, C, ldc);
+  if (m <= 0 || ncols <= 0) return 0;
+  const int tilesMN = cdiv(nbo, 128) * cdiv(ncols, 128);
+  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesMN), std::max(1, m / 256)));
+  int kchunk = cdiv(cdiv(m, splits), 16) * 16;
+  splits = cdiv(m, kchunk);
+  if ((size_t)splits * nbo * ncols > h->wp_elems) { set_err("wy_apply_outer: workspace"); return SDC_ERR_CUDA; }
+  h->gemm_sub = SDC_PROF_GEMM_W0;
+  int rc0 = gemm_tn(h, nbo, ncols, m, 1.0, f.Yp(I0), f.ldy, C, ldc, 0.0, h->Wp, nbo, nullptr, 0, 0.0,
+                    splits, kchunk, (long long)nbo * ncols);
+  h->gemm_sub = SDC_PROF_GEMM_OTHER;
+  SDC_TRY(rc0);
+  const double* Z = h->Wp;
+  if (splits > 1) {
+    ProfScope ps(h, SDC_PROF_WYRED, 8.0 * ((double)splits + 1) * nbo * ncols);
+    k_sum_partials<<<std::min(cdiv((long long)nbo * ncols, 256), 148 * 8), 256, 0, h->st>>>(
+        h->Wp, splits, (long long)nbo * ncols, (long long)nbo * ncols, h->Zb);
+    SDC_LAUNCHED(h);
+    Z = h->Zb;
+  }
+  // W = T_O^T Z (trans) or T_O Z: TN with A_s = T_O or T_O^T (both stored)
+  SDC_TRY(gemm_tn(h, nbo, ncols, nbo, 1.0, trans ? TOblk(h, I0) : TOtblk(h, I0), nbo, Z, nbo, 0.0,
+                  h->W, nbo));
+  h->gemm_sub = SDC_PROF_GEMM_UPD;
+  int rc1 = gemm_tn(h, m, ncols, nbo, -1.0, f.Ytp(I0), f.ldyt, h->W, nbo, 1.0, C, ldc);
+  h->gemm_sub = SDC_PROF_GEMM_OTHER;
+  return rc1;
+}
+
+// A (m x n, m >= n) <- Householder QR in place, two-level: 64-wide cooperative panels inside
+// nbo-wide outer blocks (inner WY updates restricted to the block), then one rank-nbo
+// trailing update per outer block.  Factors into f, T blocks into h->Tb / h->Tob.
 int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
-  for (int i0 = 0; i0 < n; i0 += NB) {
-    int nbp = std::min(NB, n - i0);
-    SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, f.Y + i0 + (long long)i0 * f.ldy,
-                  f.ldy, f.Yt + i0 + (long long)i0 * f.ldyt, f.ldyt, Tblk(h, i0), h->tau + i0));
-    if (i0 + nbp < n)
-      SDC_TRY(wy_apply(h, 1, m - i0, n - i0 - nbp, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0),
-                       nbp, A + i0 + (long long)(i0 + nbp) * lda, lda));
+  for (int I0 = 0; I0 < n; I0 += h->nbo) {
+    const int nbo = std::min(h->nbo, n - I0);
+    for (int i0 = I0; i0 < I0 + nbo; i0 += NB) {
+      const int nbp = std::min(NB, I0 + nbo - i0);
+      SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, f.Y + i0 + (long long)i0 * f.ldy,
+                    f.ldy, f.Yt + i0 + (long long)i0 * f.ldyt, f.ldyt, Tblk(h, i0), h->tau + i0,
+                    i0 - I0));
+      const int rest = (nbo > NB ? I0 + nbo : n) - (i0 + nbp);   // columns the inner WY updates
+      if (rest > 0)
+        SDC_TRY(wy_apply(h, 1, m - i0, rest, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
+                         A + i0 + (long long)(i0 + nbp) * lda, lda));
+    }
+    if (nbo > NB) {
+      SDC_TRY(build_tout(h, m, I0, nbo, f));
+      if (I0 + nbo < n)
+        SDC_TRY(wy_apply_outer(h, 1, I0, nbo, m - I0, n - I0 - nbo, f, A + I0 + (long long)(I0 + nbo) * lda,
+                               lda));
+    }
   }
   return 0;
 }
 
-// C (m x ncols) <- Q^T C  (forward over panels) for the last blocked_qr of an m x n matrix
+// C (m x ncols) <- Q^T C  (forward over outer blocks) for the last blocked_qr of an m x n matrix
 int apply_qt(sdc_handle* h, int m, int n, const Fac& f, double* C, long long ldc, int ncols) {
-  for (int i0 = 0; i0 < n; i0 += NB) {
-    int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 1, m - i0, ncols, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
-                     C + i0, ldc));
+  for (int I0 = 0; I0 < n; I0 += h->nbo) {
+    const int nbo = std::min(h->nbo, n - I0);
+    SDC_TRY(wy_apply_outer(h, 1, I0, nbo, m - I0, ncols, f, C + I0, ldc));
   }
   return 0;
 }
 
-// C (m x ncols) <- Q C  (backward over panels)
+// C (m x ncols) <- Q C  (backward over outer blocks)
 int apply_q(sdc_handle* h, int m, int n, const Fac& f, double* C, long long ldc, int ncols) {
-  int last = ((n - 1) / NB) * NB;
-  for (int i0 = last; i0 >= 0; i0 -= NB) {
-    int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 0, m - i0, ncols, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
-                     C + i0, ldc));
+  const int last = ((n - 1) / h->nbo) * h->nbo;
+  for (int I0 = last; I0 >= 0; I0 -= h->nbo) {
+    const int nbo = std::min(h->nbo, n - I0);
+    SDC_TRY(wy_apply_outer(h, 0, I0, nbo, m - I0, ncols, f, C + I0, ldc));
   }
   return 0;
 }
@@ -433,11 +531,10 @@ int apply_q(sdc_handle* h, int m, int n, const Fac& f, double* C, long long ldc,
 int form_q(sdc_handle* h, int n, const Fac& f, double* Q, long long ldq) {
   k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(Q, ldq, n, n, 1.0);
   SDC_LAUNCHED(h);
-  int last = ((n - 1) / NB) * NB;
-  for (int i0 = last; i0 >= 0; i0 -= NB) {
-    int nbp = std::min(NB, n - i0);
-    SDC_TRY(wy_apply(h, 0, n - i0, n - i0, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
-                     Q + i0 + (long long)i0 * ldq, ldq));
+  const int last = ((n - 1) / h->nbo) * h->nbo;
+  for (int I0 = last; I0 >= 0; I0 -= h->nbo) {
+    const int nbo = std::min(h->nbo, n - I0);
+    SDC_TRY(wy_apply_outer(h, 0, I0, nbo, n - I0, n - I0, f, Q + I0 + (long long)I0 * ldq, ldq));
   }
   return 0;
 }
@@ -610,6 +707,80 @@ int check_handle(sdc_handle* h) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------------
+// step phases (enqueue only; no host synchronisation)
+// ---------------------------------------------------------------------------------------
+int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const double* B, long long ldb,
+                 const double* V, long long ldv, const double* VL, long long ldvl) {
+  const long long ld = n, m = 2LL * n;
+  const bool pencil = B != nullptr;
+  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
+  h->bar_count = 0;
+  SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
+  SDC_TRY(norms(h, A, lda, n, h->scal));
+  if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
+  // A_0 = A, B_0 = B (or I); stack S = [B_0; -A_0]
+  k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->A[0], ld, A, lda, n, n, 1.0);
+  SDC_LAUNCHED(h);
+  if (pencil) k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, 1.0);
+  else k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, 1.0);
+  SDC_LAUNCHED(h);
+  k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
+  SDC_LAUNCHED(h);
+  if (pencil) {   // left IRS on (A^T, B^T)
+    SDC_TRY(transpose_rev(h, h->AL[0], ld, A, lda, n, 0));
+    SDC_TRY(transpose_rev(h, h->BL[0], ld, B, ldb, n, 0));
+    k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->SL, m, h->AL[0], ld, h->BL[0], ld, n);
+    SDC_LAUNCHED(h);
+  }
+  SDC_TRY(transpose_rev(h, h->Vt, ld, V, ldv, n, 0));                   // V^T (K-major operand)
+  if (pencil) SDC_TRY(transpose_rev(h, h->VLt, ld, VL, ldvl, n, 0));
+  return 0;
+}
+
+int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const double* B, long long ldb,
+                   double* Q, long long ldq, double* QLd, double* QL, long long ldql, double* Ahat,
+                   long long ldah, bool have_split, int cur, int max_iters) {
+  const long long ld = n;
+  const bool pencil = B != nullptr;
+  if (!have_split) {
+    SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
+    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+    SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
+  }
+  SDC_CK(cudaMemsetAsync(h->flag, 0, sizeof(int), h->st));
+  k_nonfinite<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->Ah, ld, n, h->flag);
+  SDC_LAUNCHED(h);
+  if (pencil) SDC_CK(cudaMemcpy2DAsync(QL, sizeof(double) * ldql, QLd, sizeof(double) * ld,
+                                       sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
+  if (Ahat) SDC_CK(cudaMemcpy2DAsync(Ahat, sizeof(double) * ldah, h->Ah, sizeof(double) * ld,
+                                     sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
+  SDC_CK(cudaMemcpyAsync(h->hscal, h->scal, sizeof(double) * (SCAL_HIST + (size_t)max_iters),
+                         cudaMemcpyDeviceToHost, h->st));
+  SDC_CK(cudaMemcpyAsync(h->hflags, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  SDC_CK(cudaMemcpyAsync(h->hflags + 1, h->bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  return 0;
+}
+
+int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const double* B, long long ldb,
+                  double* Q, long long ldq, double* QLd, double* QL, long long ldql, double* Ahat,
+                  long long ldah, int max_iters) {
+  // V/VL are read through the graph key's pointers; pass them via the handle's last key
+  const long long ld = n;
+  const bool pencil = B != nullptr;
+  SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, h->cur_V, h->cur_ldv, h->cur_VL, h->cur_ldvl));
+  int cur = 0;
+  for (int j = 0; j < max_iters; ++j) {
+    SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S, j,
+                     nullptr, 0));
+    if (pencil)
+      SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
+                       h->SL, -1, nullptr, 0));
+    cur ^= 1;
+  }
+  return enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, false, cur, max_iters);
+}
+
 // =======================================================================================
 // C ABI
 // =======================================================================================
@@ -648,6 +819,10 @@ int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, do
 void sdc_destroy(sdc_handle* h) {
   if (!h) return;
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  if (h->cap_st) cudaStreamDestroy(h->cap_st);
+  if (h->hscal) cudaFreeHost(h->hscal);
+  if (h->hflags) cudaFreeHost(h->hflags);
   for (void* p : h->allocs) cudaFree(p);
   delete h;
 }
@@ -694,11 +869,16 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     ALLOC(h->AL[0], nn); ALLOC(h->AL[1], nn); ALLOC(h->BL[0], nn); ALLOC(h->BL[1], nn);
     ALLOC(h->Bh, nn); ALLOC(h->QLb, nn); ALLOC(h->VLt, nn);
   }
+  if (const char* e = getenv("SDC_NBO")) h->nbo = std::max(64, std::min(256, atoi(e) / 64 * 64));
   ALLOC(h->Tb, (n / NB + 1) * NB * NB);
+  ALLOC(h->Tob, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
+  ALLOC(h->Tobt, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
+  ALLOC(h->Zb, (size_t)h->nbo * (n + 64));
+  ALLOC(h->Gb, (size_t)h->nbo * h->nbo);
   ALLOC(h->tau, n + NB);
-  h->wp_elems = (size_t)NB * (2 * (size_t)h->num_sms * TileM::BN + 2 * n + 256);
+  h->wp_elems = (size_t)256 * (2 * (size_t)h->num_sms * 128 + 2 * n + 256);
   ALLOC(h->Wp, h->wp_elems);
-  ALLOC(h->W, (size_t)NB * (n + 64));
+  ALLOC(h->W, (size_t)256 * (n + 64));
   ALLOC(h->gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
   ALLOC(h->pmA, (n / SEL_T + 1) * n);
   if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
@@ -718,6 +898,10 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   }
   if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
   if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
+  if (const char* e = getenv("SDC_GRAPH_MAX_N")) h->graph_max_n = atoi(e);
+  if (!rc && cudaMallocHost(&h->hscal, sizeof(double) * (SCAL_HIST + MAX_HIST)) != cudaSuccess) rc = SDC_ERR_NOMEM;
+  if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
+  if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
   if (rc) { sdc_destroy(h); return rc; }
   *out = h;
   return 0;
@@ -750,77 +934,80 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
   if (hist_cap < 0 || (hist_cap > 0 && !hist)) { set_err("bad hist"); return -23; }
   if (!res) { set_err("res is NULL"); return -24; }
   h->st = static_cast<cudaStream_t>(stream);
-  const long long ld = n, m = 2LL * n;
-
-  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
-  h->bar_count = 0;
-  SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
-  SDC_TRY(norms(h, A, lda, n, h->scal));
-  if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
-  // A_0 = A, B_0 = B (or I); stack S = [B_0; -A_0]
-  k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->A[0], ld, A, lda, n, n, 1.0);
-  SDC_LAUNCHED(h);
-  if (pencil) k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, 1.0);
-  else k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, 1.0);
-  SDC_LAUNCHED(h);
-  k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
-  SDC_LAUNCHED(h);
-  if (pencil) {   // left IRS on (A^T, B^T)
-    SDC_TRY(transpose_rev(h, h->AL[0], ld, A, lda, n, 0));
-    SDC_TRY(transpose_rev(h, h->BL[0], ld, B, ldb, n, 0));
-    k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->SL, m, h->AL[0], ld, h->BL[0], ld, n);
-    SDC_LAUNCHED(h);
-  }
-  SDC_TRY(transpose_rev(h, h->Vt, ld, V, ldv, n, 0));                   // V^T (K-major operand)
-  if (pencil) SDC_TRY(transpose_rev(h, h->VLt, ld, VL, ldvl, n, 0));
-  double* QLd = pencil ? h->QLb : nullptr;
+  h->cur_V = V; h->cur_ldv = ldv; h->cur_VL = VL; h->cur_ldvl = ldvl;
+  const bool pencil_ = pencil;
+  double* QLd = pencil_ ? h->QLb : nullptr;
   std::vector<double> hbuf;
   if (hist_cap > 0) hbuf.assign((size_t)hist_cap * 3, NAN);
+  int p = max_iters, conv = 0;
 
-  int cur = 0, p = max_iters, conv = 0;
-  bool have_split = false;
-  double hsel[8];
-  for (int j = 0; j < max_iters; ++j) {
-    SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S,
-                     j, nullptr, 0));
-    if (pencil)
-      SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
-                       h->SL, -1, nullptr, 0));
-    cur ^= 1;
-    if (stop_mode == SDC_STOP_RTEST && j >= 1) {
-      double ratio;
-      SDC_CK(cudaMemcpyAsync(&ratio, h->scal + SCAL_HIST + j, sizeof(double), cudaMemcpyDeviceToHost, h->st));
-      SDC_CK(cudaStreamSynchronize(h->st));
-      if (ratio <= tol) { p = j + 1; conv = 1; break; }
+  if (stop_mode == SDC_STOP_FIXED) {
+    // whole step enqueued without host syncs; captured once into a CUDA graph (n <= graph_max_n)
+    // and replayed while the call signature is unchanged
+    sdc_handle::GraphKey key;
+    key.n = n; key.max_iters = max_iters; key.nbo = h->nbo;
+    key.A = A; key.B = B; key.V = V; key.VL = VL; key.Q = Q; key.QL = QL; key.Ahat = Ahat;
+    key.lda = lda; key.ldb = ldb; key.ldv = ldv; key.ldvl = ldvl; key.ldq = ldq; key.ldql = ldql;
+    key.ldah = ldah;
+    const bool graph = n <= h->graph_max_n && !h->prof_on;
+    if (graph && h->gexec && key == h->gkey) {
+      SDC_CK(cudaGraphLaunch(h->gexec, h->st));
+      h->launches += h->glaunches;
+    } else if (graph) {
+      if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
+      const long long l0 = h->launches;
+      cudaStream_t user = h->st;           // capture on the handle's own stream (the legacy
+      h->st = h->cap_st;                   // default stream cannot be captured), launch on user's
+      SDC_CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed));
+      int rc = enqueue_fixed(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, max_iters);
+      cudaGraph_t g = nullptr;
+      cudaError_t ec = cudaStreamEndCapture(h->st, &g);
+      h->st = user;
+      if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+      if (ec != cudaSuccess) { set_err("graph capture: %s", cudaGetErrorString(ec)); return SDC_ERR_CUDA; }
+      cudaError_t ei = cudaGraphInstantiate(&h->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if (ei != cudaSuccess) { h->gexec = nullptr; set_err("graph instantiate: %s", cudaGetErrorString(ei)); return SDC_ERR_CUDA; }
+      h->gkey = key;
+      h->glaunches = h->launches - l0;
+      SDC_CK(cudaGraphLaunch(h->gexec, h->st));
+    } else {
+      SDC_TRY(enqueue_fixed(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, max_iters));
     }
-    if (stop_mode == SDC_STOP_E21) {
-      SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
-      if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
-      SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
-      have_split = true;
-      SDC_CK(cudaMemcpyAsync(hsel, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
-      SDC_CK(cudaStreamSynchronize(h->st));
-      if (j < hist_cap) { hbuf[3 * j] = hsel[0]; hbuf[3 * j + 1] = hsel[1]; }
-      if (hsel[1] <= tol) { p = j + 1; conv = 1; break; }
+  } else {
+    // RTEST / E21: host decisions between passes (one scalar D2H per pass)
+    const long long ld = n;
+    SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
+    int cur = 0;
+    bool have_split = false;
+    for (int j = 0; j < max_iters; ++j) {
+      SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S,
+                       j, nullptr, 0));
+      if (pencil)
+        SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
+                         h->SL, -1, nullptr, 0));
+      cur ^= 1;
+      if (stop_mode == SDC_STOP_RTEST && j >= 1) {
+        SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + SCAL_HIST + j, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        SDC_CK(cudaStreamSynchronize(h->st));
+        if (h->hscal[0] <= tol) { p = j + 1; conv = 1; break; }
+      }
+      if (stop_mode == SDC_STOP_E21) {
+        SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
+        if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+        SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
+        have_split = true;
+        SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        SDC_CK(cudaStreamSynchronize(h->st));
+        if (j < hist_cap) { hbuf[3 * j] = h->hscal[0]; hbuf[3 * j + 1] = h->hscal[1]; }
+        if (h->hscal[1] <= tol) { p = j + 1; conv = 1; break; }
+      }
     }
+    SDC_TRY(enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, have_split, cur, max_iters));
   }
-  if (!have_split) {
-    SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
-    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
-    SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
-  }
-  SDC_CK(cudaMemsetAsync(h->flag, 0, sizeof(int), h->st));
-  k_nonfinite<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->Ah, ld, n, h->flag);
-  SDC_LAUNCHED(h);
-  if (pencil) SDC_CK(cudaMemcpy2DAsync(QL, sizeof(double) * ldql, QLd, sizeof(double) * ld,
-                                       sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
-  if (Ahat) SDC_CK(cudaMemcpy2DAsync(Ahat, sizeof(double) * ldah, h->Ah, sizeof(double) * ld,
-                                     sizeof(double) * n, n, cudaMemcpyDeviceToDevice, h->st));
-  std::vector<double> sc(SCAL_HIST + (size_t)max_iters);
-  int flag = 0;
-  SDC_CK(cudaMemcpyAsync(sc.data(), h->scal, sizeof(double) * sc.size(), cudaMemcpyDeviceToHost, h->st));
-  SDC_CK(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-  SDC_TRY(check_barrier(h));
+  SDC_CK(cudaStreamSynchronize(h->st));
+  if (h->hflags[1]) { set_err("panel grid barrier timed out (co-residency violated?)"); return SDC_ERR_CUDA; }
+  const double* sc = h->hscal;
   for (int j = 1; j < std::min(hist_cap, p); ++j) hbuf[3 * j + 2] = sc[SCAL_HIST + j];
   if (hist_cap > 0) memcpy(hist, hbuf.data(), sizeof(double) * hbuf.size());
   res->r = (int)sc[4];
@@ -829,7 +1016,7 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
   res->metric_fro = sc[6];
   res->iters = p;
   res->converged = conv;
-  res->status = (flag || !std::isfinite(res->metric)) ? SDC_STATUS_NONFINITE
+  res->status = (h->hflags[0] || !std::isfinite(res->metric)) ? SDC_STATUS_NONFINITE
                : (res->metric <= SDC_SPLIT_ACCEPT ? SDC_STATUS_SPLIT : SDC_STATUS_NO_SPLIT);
   return 0;
 }

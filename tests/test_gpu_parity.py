@@ -258,3 +258,57 @@ def test_deterministic(handle):
     Q1, _, _, i1 = handle.split(dev(p.A), None, dev(p.V), max_iters=12)
     Q2, _, _, i2 = handle.split(dev(p.A), None, dev(p.V), max_iters=12)
     assert i1.metric == i2.metric and torch.equal(Q1, Q2)
+
+
+def _handle_with_env(sdc, n_max, pencil=False, **env):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        for k, v in env.items():
+            os.environ[k] = str(v)
+        return sdc.Handle(n_max, pencil=pencil)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("nbo", [64, 128, 256])
+def test_outer_block_widths_parity(orc, sdc, nbo):
+    # two-level blocking (64-wide panels inside nbo-wide compact-WY blocks) at a ragged
+    # size: every outer width gives the same invariants as the oracle
+    h = _handle_with_env(sdc, 600, SDC_NBO=nbo)
+    p = inputs.make_config(2, n=600)
+    Q, _, Ah, info, o = run_both(orc, h, p)
+    assert_parity(o, Q, info, p.A, p.n, Ah)
+    assert info.k == p.expected_k
+
+
+def test_blocked_qr_two_level_r_unique(orc, sdc):
+    # R of the two-level QR equals the oracle's (unique with diag >= 0) at 2n x n, n = 700
+    h = _handle_with_env(sdc, 700, SDC_NBO=256)
+    s = np.random.default_rng(77).standard_normal((1400, 700))
+    q, r = h.qr(dev(s))
+    _, r_o = orc.qr_signed(s)
+    assert np.allclose(host(r), r_o, rtol=0, atol=1e-12 * np.abs(r_o).max() * np.sqrt(700))
+    assert orth_err(host(q)) <= 64 * 700 * EPS
+
+
+def test_graph_replay_matches_direct(sdc):
+    # the FIXED-mode step captured as one CUDA graph gives bit-identical results to the
+    # directly launched sequence, and replays (same pointers) stay identical
+    p = inputs.make_config(1)
+    hg = _handle_with_env(sdc, 64, SDC_GRAPH_MAX_N=4096)
+    hd = _handle_with_env(sdc, 64, SDC_GRAPH_MAX_N=0)
+    A, V = dev(p.A), dev(p.V)
+    Qg = sdc.empty_colmajor(64, 64, A.device)
+    Qd = sdc.empty_colmajor(64, 64, A.device)
+    _, _, _, ig1 = hg.split(A, None, V, max_iters=12, Q=Qg)
+    q1 = Qg.clone()
+    _, _, _, ig2 = hg.split(A, None, V, max_iters=12, Q=Qg)   # replay
+    _, _, _, idd = hd.split(A, None, V, max_iters=12, Q=Qd)
+    assert torch.equal(q1, Qg) and torch.equal(Qg, Qd)
+    assert ig1.metric == ig2.metric == idd.metric and ig1.r == idd.r
+    assert hg.launches > 0
