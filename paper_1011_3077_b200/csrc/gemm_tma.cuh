@@ -36,9 +36,13 @@ struct TmaGemmArgs {
   long long c_zstride;    // element stride between z-slices of C
 };
 
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1>
+// CPRE: the C tile (beta != 0) is brought into shared memory by TMA at kernel start, in
+// 16-row boxes with the same 128B swizzle, so the epilogue of short-K updates (K <= 256,
+// C -= Y W) reads C on-chip instead of exposing HBM/L2 latency after the main loop.
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1, bool CPRE_ = false>
 struct TmaTile {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr bool CPRE = CPRE_;
   static constexpr int BK = 16;                       // one 128-byte swizzle row of doubles
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int CWARPS = WARPS_M * WARPS_N;    // all warps consume
@@ -46,7 +50,8 @@ struct TmaTile {
   static constexpr int MI = WM / 8, NI = WN / 8;
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+  static constexpr int C_BYTES = CPRE ? BM * BN * 8 : 0;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + C_BYTES + 2 * STAGES * 8 + 16 + 1024;
 };
 
 SDC_DEV void mbar_init(uint64_t* bar, unsigned count) {
@@ -82,12 +87,14 @@ SDC_DEV int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
 gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const TmaGemmArgs g) {
+                   const __grid_constant__ CUtensorMap tmC, const TmaGemmArgs g) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  double* sC = reinterpret_cast<double*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES + T::C_BYTES);
   uint64_t* empty = full + T::STAGES;
+  uint64_t* cbar = empty + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * T::BM, n0 = blockIdx.y * T::BN;
   const int kbeg = blockIdx.z * g.kchunk;
@@ -99,6 +106,7 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       mbar_init(full + s, 1);
       mbar_init(empty + s, T::CWARPS);
     }
+    if (T::CPRE) mbar_init(cbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -113,7 +121,14 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     tma_load_2d(st, &tmA, k, m0, full + s);
     tma_load_2d(st + T::A_BYTES, &tmB, k, n0, full + s);
   };
-  if (g.beta != 0.0) {   // warm L2 with this CTA's C tile: one prefetch per 128-byte line
+  const bool cpre = T::CPRE && g.beta != 0.0;
+  if (cpre && threadIdx.x == 0) {   // C tile -> smem: BM/16 boxes of 16 rows x BN columns
+    mbar_expect_tx(cbar, T::C_BYTES);
+#pragma unroll 1
+    for (int b = 0; b < T::BM / 16; ++b)
+      tma_load_2d(sC + b * 16 * T::BN, &tmC, m0 + 16 * b, n0, cbar);
+  }
+  if (!cpre && g.beta != 0.0) {   // warm L2 with this CTA's C tile: one prefetch per 128-byte line
     const double* Cz = g.C + (long long)blockIdx.z * g.c_zstride;
     constexpr int LPC = (T::BM * 8 + 127) / 128;            // lines per column
     for (int e = threadIdx.x; e < LPC * T::BN; e += T::THREADS) {
@@ -168,6 +183,7 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   double* __restrict__ D2 = g.D2;
   const int c0 = frag_row(2 * fc), c1 = frag_row(2 * fc + 1);
   const bool use_beta = g.beta != 0.0;
+  if (cpre) mbar_wait(cbar, 0);
 #pragma unroll
   for (int i = 0; i < T::MI; ++i) {
     const int m = m0 + aoff[i];
@@ -178,8 +194,15 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
       for (int j = 0; j < T::NI; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int n = n0 + wn * T::WN + j * 8 + (h ? c1 : c0);
-          old[j][h] = (mok && n < g.N) ? C[m + (long long)n * g.ldc] : 0.0;
+          const int nl = wn * T::WN + j * 8 + (h ? c1 : c0);   // tile-local column
+          const int n = n0 + nl;
+          if (cpre) {   // smem box b = aoff/16 holds rows 16b..16b+15 as [n][16 m] swizzled
+            const int ml = aoff[i];
+            old[j][h] = sC[(ml >> 4) * 16 * T::BN + nl * 16 +
+                           (((((ml & 15) >> 1) ^ (nl & 7)) << 1) | (ml & 1))];
+          } else {
+            old[j][h] = (mok && n < g.N) ? C[m + (long long)n * g.ldc] : 0.0;
+          }
         }
     }
 #pragma unroll

@@ -82,6 +82,8 @@ struct sdc_handle {
   unsigned long long* dbg = nullptr;   // debug counters (sdc_debug_counters)
   bool dbg_on = false;
   int panel_rows = 128;                // target rows per panel CTA
+  bool cluster_ok = false;             // 16-CTA clusters usable for the panel kernel
+  int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width (multiple of 64)
   double *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr, *Gb = nullptr;
   // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
@@ -204,6 +206,7 @@ using TmaL = TmaTile<128, 128, 64, 32, 6>;      // 8 consumer warps, 192 KB ring
 using TmaM = TmaTile<64, 128, 32, 32, 6>;       // M <= 64 (W0 = Y^T C), 8 consumer warps
 using TmaS = TmaTile<64, 64, 32, 32, 6>;        // small grids, 4 consumer warps
 using TmaU = TmaTile<128, 64, 64, 32, 4, 2>;    // rank-nb updates: 2 CTAs/SM, epilogue overlap
+using TmaC = TmaTile<128, 128, 64, 32, 3, 1, true>;  // K <= 256 updates, C tile prefetched by TMA
 
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
@@ -283,14 +286,22 @@ int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B,
                                 (int)T::SMEM));
     attr_set = 1;
   }
-  CUtensorMap tA, tB;
+  CUtensorMap tA, tB, tC;
   if (!make_tmap(&tA, A, g.K, g.M, lda, T::BM) || !make_tmap(&tB, B, g.K, g.N, ldb, T::BN)) {
     set_err("cuTensorMapEncodeTiled failed");
     return SDC_ERR_CUDA;
   }
+  if (T::CPRE) {   // C as a 2-D tensor: rows = M (contiguous), cols = N; 16-row boxes
+    if (!make_tmap(&tC, g.C, g.M, g.N, g.ldc, T::BN)) {
+      set_err("cuTensorMapEncodeTiled (C) failed");
+      return SDC_ERR_CUDA;
+    }
+  } else {
+    tC = tA;
+  }
   dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
   ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
-  gemm_tn_tma_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, g);
+  gemm_tn_tma_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, tC, g);
   SDC_LAUNCHED(h);
   return 0;
 }
@@ -307,16 +318,20 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (tma) {
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride};
     int v = gemm_variant_override();
+    const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
       if (M <= 64) v = 1;
       else if (K <= 128) v = 3;
+      else if (K <= 256) v = 3;   // short-K update: 2 CTAs/SM overlap epilogue and prologue
       else if ((long long)cdiv(M, 128) * cdiv(N, 128) * splits >= h->num_sms) v = 0;
       else v = 2;
     }
+    if (v == 4 && !cok) v = 0;
     switch (v) {
       case 0: return launch_tma_t<TmaL>(h, A, lda, B, ldb, g, splits);
       case 1: return launch_tma_t<TmaM>(h, A, lda, B, ldb, g, splits);
       case 2: return launch_tma_t<TmaS>(h, A, lda, B, ldb, g, splits);
+      case 4: return launch_tma_t<TmaC>(h, A, lda, B, ldb, g, splits);
       default: return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
     }
   }
@@ -334,6 +349,23 @@ int gemm_general(sdc_handle* h, bool ta, bool tb, int M, int N, int K, double al
   if (!ta && !tb) return launch_gemm_tile<false, false>(h, g, 1);
   if (!ta && tb) return launch_gemm_tile<false, true>(h, g, 1);
   return launch_gemm_tile<true, true>(h, g, 1);
+}
+
+// split-K factor for a tall-K GEMM with `tiles` output tiles: at least ~2 waves of CTAs,
+// K slices >= 256, and the fewest splits whose last wave is >= 90% full (wave quantisation)
+int pick_splits(sdc_handle* h, int tiles, int K, long long cap) {
+  const int smax = (int)std::max(1LL, std::min<long long>(std::min(K / 256, 64), cap));
+  const int P = h->num_sms;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= smax; ++s) {
+    const long long ctas = (long long)tiles * s;
+    const long long waves = (ctas + P - 1) / P;
+    const double eff = (double)ctas / (double)(waves * P);
+    if (ctas >= 2LL * P && eff >= 0.9) return s;
+    if (eff > best_eff + 1e-9 || (ctas < 2LL * P && s == smax)) { best_eff = eff; best = s; }
+  }
+  return best;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -386,32 +418,51 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
 // ---------------------------------------------------------------------------------------
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
-  int G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
+  // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange), else a cooperative grid
+  const bool cluster = h->cluster_ok && m <= h->cluster_max_rows;
+  int G = cluster ? std::min(16, std::max(1, cdiv(m, h->panel_rows)))
+                  : std::min(h->num_sms, std::max(1, m / h->panel_rows));
   int rows_per = cdiv(m, G);
   if (rows_per < nb) {
     rows_per = nb;
     G = cdiv(m, rows_per);
   }
   size_t smem = panel_smem_bytes(rows_per);
-  static size_t attr_smem = 0;
-  if (smem > attr_smem) {
-    cudaError_t e = cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static size_t attr_smem[2] = {0, 0};
+  if (smem > attr_smem[cluster]) {
+    cudaError_t e = cudaFuncSetAttribute(cluster ? panel_qr_kernel_t<true> : panel_qr_kernel_t<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       set_err("panel: %d rows per CTA need %zu B of shared memory (n too large): %s", rows_per,
               smem, cudaGetErrorString(e));
       return SDC_ERR_NOT_SUPPORTED;
     }
-    attr_smem = smem;
+    attr_smem[cluster] = smem;
   }
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
               rows_per, h->dbg_on ? h->dbg : nullptr, zero_above};
-  void* args[] = {&a};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
-  SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel, dim3(G), dim3(PANEL_THREADS),
-                                     args, smem, h->st));
+  if (cluster) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(PANEL_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = G;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SDC_CK(cudaLaunchKernelEx(&cfg, panel_qr_kernel_t<true>, a));
+  } else {
+    void* args[] = {&a};
+    SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel_t<false>, dim3(G),
+                                       dim3(PANEL_THREADS), args, smem, h->st));
+    h->bar_count += (unsigned long long)G * nb;
+  }
   h->launches++;
-  h->bar_count += (unsigned long long)G * nb;
   return 0;
 }
 
@@ -456,7 +507,7 @@ int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, 
                                  nbo, C, ldc);
   if (m <= 0 || ncols <= 0) return 0;
   const int tilesMN = cdiv(nbo, 128) * cdiv(ncols, 128);
-  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesMN), std::max(1, m / 256)));
+  int splits = pick_splits(h, tilesMN, m, (long long)(h->wp_elems / ((size_t)nbo * ncols)));
   int kchunk = cdiv(cdiv(m, splits), 16) * 16;
   splits = cdiv(m, kchunk);
   if ((size_t)splits * nbo * ncols > h->wp_elems) { set_err("wy_apply_outer: workspace"); return SDC_ERR_CUDA; }
@@ -899,6 +950,32 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
   if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
   if (const char* e = getenv("SDC_GRAPH_MAX_N")) h->graph_max_n = atoi(e);
+  if (const char* e = getenv("SDC_CLUSTER_MAX_ROWS")) h->cluster_max_rows = atoi(e);
+  if (!rc) {   // non-portable cluster size 16 for the small-panel kernel (if the part allows it)
+    int cl = 0;
+    cudaDeviceGetAttribute(&cl, cudaDevAttrClusterLaunch, device);
+    if (cl && cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                   1) == cudaSuccess) {
+      cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)panel_smem_bytes(cdiv(h->cluster_max_rows, 16)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(16);
+      cfg.blockDim = dim3(PANEL_THREADS);
+      cfg.dynamicSmemBytes = panel_smem_bytes(cdiv(h->cluster_max_rows, 16));
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 16;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, panel_qr_kernel_t<true>, &cfg) == cudaSuccess && ncl >= 1)
+        h->cluster_ok = true;
+      cudaGetLastError();
+    }
+    if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = false;
+  }
   if (!rc && cudaMallocHost(&h->hscal, sizeof(double) * (SCAL_HIST + MAX_HIST)) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;

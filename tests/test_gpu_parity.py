@@ -312,3 +312,13 @@ def test_graph_replay_matches_direct(sdc):
     assert torch.equal(q1, Qg) and torch.equal(Qg, Qd)
     assert ig1.metric == ig2.metric == idd.metric and ig1.r == idd.r
     assert hg.launches > 0
+
+
+@pytest.mark.parametrize("env", [{"SDC_NO_CLUSTER": 1}, {"SDC_CLUSTER_MAX_ROWS": 4096}])
+def test_panel_exchange_modes_parity(orc, sdc, env):
+    # cluster/DSMEM panel (small panels) and cooperative-grid/L2 panel give the same
+    # invariants on config 2's recipe at n = 600
+    h = _handle_with_env(sdc, 600, **env)
+    p = inputs.make_config(2, n=600)
+    Q, _, Ah, info, o = run_both(orc, h, p)
+    assert_parity(o, Q, info, p.A, p.n, Ah)
