@@ -28,7 +28,16 @@
 namespace sdc {
 
 constexpr int PANEL_NB = 64;        // max panel width
-constexpr int PANEL_THREADS = 256;
+constexpr int PANEL_THREADS = 512;
+constexpr int PANEL_RG = PANEL_THREADS / PANEL_NB;   // row groups (8)
+
+// fixed-order sum of the PANEL_RG row-group partials of column j
+SDC_DEV double sum_groups(const double* red, int j) {
+  double t = 0.0;
+#pragma unroll
+  for (int g = 0; g < PANEL_RG; ++g) t += red[g * 64 + j];
+  return t;
+}
 constexpr int PANEL_LD = PANEL_NB + 1;  // smem row stride (doubles) of the local panel
 
 struct PanelArgs {
@@ -79,24 +88,25 @@ panel_qr_kernel_t(const PanelArgs a) {
   const int r1 = min(a.m, r0 + a.rows_per);
   const int R = max(0, r1 - r0);
   double* Ps = sm;                                  // R x PANEL_LD, row-major local block
-  double* red = Ps + (size_t)a.rows_per * PANEL_LD; // 4 x PANEL_NB
-  double* totb = red + 4 * PANEL_NB;                // 2 x PANEL_NB (by column parity)
+  double* red = Ps + (size_t)a.rows_per * PANEL_LD; // PANEL_RG x PANEL_NB
+  double* totb = red + (PANEL_RG + 1) * PANEL_NB;                // 2 x PANEL_NB (by column parity)
   double* drowb = totb + 2 * PANEL_NB;              // 2 x PANEL_NB
   double* sc = drowb + 2 * PANEL_NB;                // PANEL_NB: v_i = sc[i] * x_i
   double* tauv = sc + PANEL_NB;                     // PANEL_NB
-  double* Ts = tauv + PANEL_NB;                     // PANEL_NB x PANEL_NB (CTA 0), col-major
-  double* xch = Ts + PANEL_NB * PANEL_NB;           // cluster mode: 2 x {partials, row k}
+  double* Ts = tauv + PANEL_NB;                     // PANEL_NB x PANEL_NB (T CTA), col-major
+  double* xch = Ts + PANEL_NB * PANEL_NB;           // cluster mode: 2 x {-, row k, 16 partials}
 
   // load the CTA's row block
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {
     int j = e / R, r = e % R;                       // coalesced along rows
     Ps[r * PANEL_LD + j] = a.P[(long long)(r0 + r) + (long long)j * a.ldp];
   }
-  if (cta == 0)
+  const int tcta = G - 1;                          // builds T (fewest rows: off the critical path)
+  if (cta == tcta)
     for (int e = tid; e < PANEL_NB * PANEL_NB; e += PANEL_THREADS) Ts[e] = 0.0;
   __syncthreads();
 
-  const int jj = tid & (PANEL_NB - 1), rg = tid >> 6;  // column lane, row group (0..3)
+  const int jj = tid & (PANEL_NB - 1), rg = tid / PANEL_NB;  // column lane, row group
   const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
   unsigned long long ph[4] = {0, 0, 0, 0}, t0 = 0, t1;
   for (int k = 0; k < nb; ++k) {
@@ -107,70 +117,71 @@ panel_qr_kernel_t(const PanelArgs a) {
     if (jj < nb) {
       double s1 = 0.0;
       int r = lbeg + rg;
-      for (; r + 4 < R; r += 8) {
+      for (; r + PANEL_RG < R; r += 2 * PANEL_RG) {
         s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
-        s1 = fma(Ps[(r + 4) * PANEL_LD + k], Ps[(r + 4) * PANEL_LD + jj], s1);
+        s1 = fma(Ps[(r + PANEL_RG) * PANEL_LD + k], Ps[(r + PANEL_RG) * PANEL_LD + jj], s1);
       }
       if (r < R) s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
       s += s1;
     }
     red[rg * PANEL_NB + jj] = s;
-    if (cta == 0 && k > 0)   // T column of the previous step (its inputs are double-buffered)
+    if (cta == tcta && k > 0)   // T column of the previous step (inputs double-buffered)
       panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
                      sc, tauv);
     __syncthreads();
     double* gb = a.gbuf + (size_t)(k & 1) * (G + 1) * PANEL_NB;
-    double* xp = xch + (k & 1) * 2 * PANEL_NB;        // cluster mode exchange slot
+    double* xp = xch + (k & 1) * 18 * PANEL_NB;       // cluster mode exchange slot
     if (tid < nb) {
-      double p = ((red[tid] + red[PANEL_NB + tid]) + red[2 * PANEL_NB + tid]) + red[3 * PANEL_NB + tid];
+      double p = sum_groups(red, tid);
       if constexpr (CLUSTER) {
-        xp[tid] = p;
-        if (cta == 0) xp[PANEL_NB + tid] = Ps[k * PANEL_LD + tid];                   // row k
+        red[PANEL_RG * PANEL_NB + tid] = p;       // staged for the push below
       } else {
         __stcg(gb + (size_t)cta * PANEL_NB + tid, p);
         if (cta == 0) __stcg(gb + (size_t)G * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);  // row k
       }
+    }
+    if constexpr (CLUSTER) {
+      // push: every CTA writes its partial vector (and CTA 0 row k) into every peer's
+      // exchange slot, so after the cluster barrier all reads are local
+      __syncthreads();
+      auto cl = cooperative_groups::this_cluster();
+      if (jj < nb)
+        for (int d = rg; d < G; d += PANEL_RG) {
+          double* dst = cl.map_shared_rank(xp, d);
+          dst[2 * PANEL_NB + cta * PANEL_NB + jj] = red[PANEL_RG * PANEL_NB + jj];
+          if (cta == 0) dst[PANEL_NB + jj] = Ps[k * PANEL_LD + jj];
+        }
     }
     if (timed) { t1 = clock64(); ph[0] += t1 - t0; t0 = t1; }
     if constexpr (CLUSTER) cooperative_groups::this_cluster().sync();
     else grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
     if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
     const double* row0;                                 // row k of the panel (owned by CTA 0)
-    if constexpr (CLUSTER) row0 = cooperative_groups::this_cluster().map_shared_rank(xp, 0) + PANEL_NB;
+    if constexpr (CLUSTER) row0 = xp + PANEL_NB;
     else row0 = gb + (size_t)G * PANEL_NB;
     // (b) every CTA sums the per-CTA partials in the same fixed order
     if constexpr (CLUSTER) {
       double t = 0.0;
       if (jj < nb) {
-        auto cl = cooperative_groups::this_cluster();
-        double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int c = rg + 4 * u;
-          v[u] = c < G ? cl.map_shared_rank(xp, c)[jj] : 0.0;
+        for (int u = 0; u < 16 / PANEL_RG; ++u) {
+          const int c = rg + PANEL_RG * u;
+          t += c < G ? xp[2 * PANEL_NB + c * PANEL_NB + jj] : 0.0;
         }
-        t = ((v[0] + v[1]) + v[2]) + v[3];
       }
       red[rg * PANEL_NB + jj] = t;
     } else {
       double t = 0.0;
       if (jj < nb) {
         int c = rg;
-        for (; c + 60 < G; c += 64) {   // batch 16 independent L2 loads, add in order
-          double v[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) v[u] = __ldcg(gb + (size_t)(c + 4 * u) * PANEL_NB + jj);
-#pragma unroll
-          for (int u = 0; u < 16; ++u) t += v[u];
-        }
-        for (; c + 28 < G; c += 32) {
+        for (; c + 7 * PANEL_RG < G; c += 8 * PANEL_RG) {   // 8 independent L2 loads in flight
           double v[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __ldcg(gb + (size_t)(c + 4 * u) * PANEL_NB + jj);
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(gb + (size_t)(c + PANEL_RG * u) * PANEL_NB + jj);
 #pragma unroll
           for (int u = 0; u < 8; ++u) t += v[u];
         }
-        for (; c < G; c += 4) t += __ldcg(gb + (size_t)c * PANEL_NB + jj);
+        for (; c < G; c += PANEL_RG) t += __ldcg(gb + (size_t)c * PANEL_NB + jj);
       }
       red[rg * PANEL_NB + jj] = t;
     }
@@ -178,7 +189,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     if (timed) { t1 = clock64(); ph[2] += t1 - t0; t0 = t1; }
     // (c) reflector of column k, computed redundantly by every thread (identical values)
     const double alpha = CLUSTER ? row0[k] : __ldcg(row0 + k);
-    const double sigma = ((red[k] + red[PANEL_NB + k]) + red[2 * PANEL_NB + k]) + red[3 * PANEL_NB + k];
+    const double sigma = sum_groups(red, k);
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (sigma != 0.0) {
       const double nrm = sqrt(alpha * alpha + sigma);
@@ -187,7 +198,7 @@ panel_qr_kernel_t(const PanelArgs a) {
       scale = 1.0 / (alpha - beta);
     }
     if (jj < nb) {
-      const double totj = ((red[jj] + red[PANEL_NB + jj]) + red[2 * PANEL_NB + jj]) + red[3 * PANEL_NB + jj];
+      const double totj = sum_groups(red, jj);
       const double drowj = CLUSTER ? row0[jj] : __ldcg(row0 + jj);
       if (rg == 0) { totb[(k & 1) * PANEL_NB + jj] = totj; drowb[(k & 1) * PANEL_NB + jj] = drowj; }
       if (jj > k) {
@@ -195,7 +206,7 @@ panel_qr_kernel_t(const PanelArgs a) {
         const double w = tau * fma(scale, totj, drowj);
         const double ws = w * scale;
 #pragma unroll 4
-        for (int r = lbeg + rg; r < R; r += 4)
+        for (int r = lbeg + rg; r < R; r += PANEL_RG)
           Ps[r * PANEL_LD + jj] = fma(-ws, Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj]);
         if (cta == 0 && rg == 0) Ps[k * PANEL_LD + jj] -= w;      // diagonal row k
       }
@@ -208,7 +219,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     __syncthreads();
     if (timed) { t1 = clock64(); ph[3] += t1 - t0; }
   }
-  if (cta == 0) {
+  if (cta == tcta) {
     panel_t_column(Ts, nb - 1, totb + ((nb - 1) & 1) * PANEL_NB, drowb + ((nb - 1) & 1) * PANEL_NB,
                    sc, tauv);
   }
@@ -235,11 +246,12 @@ panel_qr_kernel_t(const PanelArgs a) {
     double v = gr > j ? sc[j] * Ps[r * PANEL_LD + j] : (gr == j ? 1.0 : 0.0);
     a.Yt[(long long)j + (long long)gr * a.ldyt] = v;
   }
-  if (cta == 0) {
+  if (cta == tcta)
     for (int e = tid; e < nb * nb; e += PANEL_THREADS) {
       int j = e / nb, i = e % nb;
       a.T[e] = Ts[j * PANEL_NB + i];
     }
+  if (cta == 0) {
     // rows [-zero_above, 0) of this panel's Y columns belong to the outer block: zeros
     for (int e = tid; e < a.zero_above * nb; e += PANEL_THREADS) {
       int j = e / a.zero_above, r = e % a.zero_above - a.zero_above;
@@ -253,8 +265,8 @@ panel_qr_kernel_t(const PanelArgs a) {
 }
 
 inline size_t panel_smem_bytes(int rows_per) {
-  return sizeof(double) * ((size_t)rows_per * PANEL_LD + 4 * PANEL_NB + 4 * PANEL_NB + 2 * PANEL_NB +
-                           PANEL_NB * PANEL_NB + 4 * PANEL_NB);
+  return sizeof(double) * ((size_t)rows_per * PANEL_LD + (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB +
+                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB);
 }
 
 }  // namespace sdc

@@ -93,7 +93,9 @@ def test_irs_pass_vs_oracle(orc, handle, n):
     assert np.allclose(r, r_o, rtol=0, atol=1e-12 * np.abs(r_o).max())
     m_gpu = np.linalg.solve(ao, bo)
     m_ora = np.linalg.solve(ao_o, bo_o)
-    assert np.linalg.norm(m_gpu - m_ora) <= 1e-10 * np.linalg.norm(m_ora)
+    # both equal (A^{-1}B)^2 up to rounding amplified by the conditioning of A_{j+1}
+    kappa = np.linalg.cond(ao_o)
+    assert np.linalg.norm(m_gpu - m_ora) <= 1e-14 * n * kappa * np.linalg.norm(m_ora)
     # Q12^T B_j = Q22^T A_j means the new pencil is left-equivalent:
     # [A_{j+1}; B_{j+1}] has orthonormal-complement structure -> same singular values
     sv = np.linalg.svd(np.vstack([ao, bo]), compute_uv=False)
