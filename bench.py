@@ -45,6 +45,28 @@ def flop_model(n: int, passes: int, pencil: bool = False, monitor: bool = False)
     return (40.0 * passes / 3.0 + 12.0) * n3
 
 
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a per-rank time over all ranks (the bench contract's multi-GPU timing)."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(ms_per_step_max: float, world: int) -> float:
+    """Whole-job split steps/s of `world` independent replicas ("replicas only")."""
+    return world / (ms_per_step_max / 1e3)
+
+
+def run_config(cfg_name: str, n: int, passes: int, stop: str, world: int) -> dict:
+    return {"workload": cfg_name, "n": n, "passes": passes, "stop": stop,
+            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "l2": "inputs and working set (>= 2 GiB per matrix) exceed L2; no flush needed"}
+
+
 def hbm_peak():
     try:
         return float(json.load(open(MEASURED))["hbm_gbs"]), "measured"
@@ -133,7 +155,7 @@ def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 1536
     return total, threads, sample, time.perf_counter() - t_spent
 
 
-def run_reference(args, cfg_name, n, passes, pencil, rank, world):
+def run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg=5):
     if rank != 0:
         return 0
     steps = []
@@ -149,7 +171,7 @@ def run_reference(args, cfg_name, n, passes, pencil, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg_name, "n": n, "passes": passes},
+            "config": run_config(cfg_name, n, passes, "e21" if cfg == 3 else "fixed", 1),
             "tflops_effective": flop_model(n, passes, pencil) / t / 1e12,
             "cpu_baseline": {"value": val, "unit": "split steps/s", "cores": threads,
                              "kind": "oracle", "sample": sample + " (extrapolated)"},
@@ -185,7 +207,7 @@ def main():
 
     if args.impl == "reference":
         passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30}[cfg]
-        return run_reference(args, cfg_name, n, passes, pencil, rank, world)
+        return run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg)
 
     import numpy as np
     import torch
@@ -245,13 +267,10 @@ def main():
     prof_steps = args.steps if live_prof else 1
     prof = {c: h.profile_read(c) for c in range(7)}
     h.profile(False)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, dev)
     info = infos[-1]
     F = flop_model(n, info.iters, pencil, monitor=(stop == "e21"))
-    value = world / (ms / 1e3)
+    value = replica_throughput(ms, world)
     tflops = F / (ms / 1e3) / 1e12
 
     # ---- end to end: host buffers through the C ABI, copies inside the timed region ----
@@ -274,13 +293,9 @@ def main():
             h.split_host(hA, hB, hV, hVL, max_iters=passes, tol=p.tol, stop=stop, Q=hQ, QL=hQL)
         e1.record(st)
         barrier()
-        ms_e2e = e0.elapsed_time(e1) / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([ms_e2e], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e2e = float(t.item())
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
         nin = 2 + (2 if pencil else 0)
-        e2e = {"value": world / (ms_e2e / 1e3), "unit": "split steps/s",
+        e2e = {"value": replica_throughput(ms_e2e, world), "unit": "split steps/s",
                "h2d_bytes_per_step": nin * n * n * 8, "d2h_bytes_per_step": (2 if pencil else 1) * n * n * 8,
                "ms_per_step": ms_e2e, "steps": args.e2e_steps}
 
@@ -323,9 +338,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": cfg_name, "n": n, "passes": info.iters, "stop": stop,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs and working set (>= 2 GiB per matrix) exceed L2; no flush needed"},
+            "config": run_config(cfg_name, n, info.iters, stop, world),
             "tflops_effective": tflops, "fp64_peak_tflops": FP64_PEAK_TFLOPS,
             "frac_of_fp64_peak": tflops / FP64_PEAK_TFLOPS,
             "frac_of_clock_adjusted_peak": (tflops / (FP64_PEAK_TFLOPS * clocks["sm_mhz"] / 1965.0))

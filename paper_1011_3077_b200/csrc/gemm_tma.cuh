@@ -96,7 +96,18 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint64_t* empty = full + T::STAGES;
   uint64_t* cbar = empty + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * T::BM, n0 = blockIdx.y * T::BN;
+  // grouped rasterisation (no split-K): consecutive CTAs sweep GROUP M-tiles x all N-tiles
+  // column by column, so the ~148 co-resident CTAs share A and B tiles in L2
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (gridDim.z == 1 && gridDim.x > 16) {
+    constexpr int GROUP = 16;
+    const int nm = gridDim.x, nn = gridDim.y;
+    const int pid = blockIdx.x + blockIdx.y * nm;
+    const int width = GROUP * nn, first = (pid / width) * GROUP, gs = min(nm - first, GROUP);
+    bx = first + (pid % width) % gs;
+    by = (pid % width) / gs;
+  }
+  const int m0 = bx * T::BM, n0 = by * T::BN;
   const int kbeg = blockIdx.z * g.kchunk;
   const int kend = min(g.K, kbeg + g.kchunk);
   const int ktiles = kend > kbeg ? (kend - kbeg + T::BK - 1) / T::BK : 0;
@@ -155,6 +166,11 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   for (int i = 0; i < T::MI; ++i) aoff[i] = wm * T::WM + i * 8 + fr;
 #pragma unroll
   for (int j = 0; j < T::NI; ++j) boff[j] = wn * T::WN + j * 8 + fr;
+  // swz(row, 4kq + fc) = row*16 + ktab[kq] for every fragment row (row % 8 == fr)
+  int ktab[T::BK / 4];
+#pragma unroll
+  for (int kq = 0; kq < T::BK / 4; ++kq) ktab[kq] = swz(fr, 4 * kq + fc) - fr * 16;
+  const int abase = (wm * T::WM + fr) * 16, bbase = (wn * T::WN + fr) * 16;
 
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % T::STAGES;
@@ -163,12 +179,16 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
     const double* sA = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES);
     const double* sB = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES + T::A_BYTES);
 #pragma unroll
-    for (int kk = 0; kk < T::BK; kk += 4) {
+    for (int kq = 0; kq < T::BK / 4; ++kq) {
+      // every fragment row r has r % 8 == fr, so the swizzled in-row offset depends only on
+      // (kq, lane): rows differ by compile-time multiples of 128 doubles (LDS immediates)
       double af[T::MI], bf[T::NI];
+      const double* pa = sA + abase + ktab[kq];
+      const double* pb = sB + bbase + ktab[kq];
 #pragma unroll
-      for (int i = 0; i < T::MI; ++i) af[i] = sA[swz(aoff[i], kk + fc)];
+      for (int i = 0; i < T::MI; ++i) af[i] = pa[i * 128];
 #pragma unroll
-      for (int j = 0; j < T::NI; ++j) bf[j] = sB[swz(boff[j], kk + fc)];
+      for (int j = 0; j < T::NI; ++j) bf[j] = pb[j * 128];
 #pragma unroll
       for (int i = 0; i < T::MI; ++i)
 #pragma unroll
