@@ -240,4 +240,163 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Persistent variant: gridDim.x CTAs (<= resident capacity) walk the tile sequence
+// t = blockIdx.x, blockIdx.x + gridDim.x, ... (grouped rasterisation inside each K-slice);
+// the TMA ring runs continuously across tiles, so the next tile's first K slices are in
+// flight while the current tile's epilogue runs (hides the prologue of short-K updates).
+// ---------------------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(T::THREADS, T::MINB)
+gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmB, const TmaGemmArgs g) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  uint64_t* empty = full + T::STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tx = (g.M + T::BM - 1) / T::BM, ty = (g.N + T::BN - 1) / T::BN;
+  const int tz = (g.K + g.kchunk - 1) / g.kchunk;
+  const int ntiles = tx * ty * tz;
+
+  auto decode = [&](int t, int& m0, int& n0, int& z) {
+    z = t / (tx * ty);
+    const int pid = t - z * tx * ty;
+    constexpr int GROUP = 16;
+    const int width = GROUP * ty, first = (pid / width) * GROUP, gs = min(tx - first, GROUP);
+    m0 = (first + (pid % width) % gs) * T::BM;
+    n0 = ((pid % width) / gs) * T::BN;
+  };
+  auto ktiles_of = [&](int z) {
+    const int kb = z * g.kchunk, ke = min(g.K, kb + g.kchunk);
+    return ke > kb ? (ke - kb + T::BK - 1) / T::BK : 0;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < T::STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, T::CWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // producer cursor (thread 0): the (tile, k-slice) stream of this CTA
+  const bool producer = (threadIdx.x == 0);
+  int p_tile = blockIdx.x, p_kt = 0, p_nk = 0, p_m0 = 0, p_n0 = 0, p_kb = 0;
+  unsigned g_issue = 0;
+  if (producer && p_tile < ntiles) {
+    int z;
+    decode(p_tile, p_m0, p_n0, z);
+    p_nk = ktiles_of(z);
+    p_kb = z * g.kchunk;
+  }
+  auto issue_next = [&]() {
+    while (p_tile < ntiles && p_kt >= p_nk) {
+      p_tile += gridDim.x;
+      p_kt = 0;
+      if (p_tile < ntiles) {
+        int z;
+        decode(p_tile, p_m0, p_n0, z);
+        p_nk = ktiles_of(z);
+        p_kb = z * g.kchunk;
+      }
+    }
+    if (p_tile >= ntiles) return;
+    const int s = g_issue % T::STAGES;
+    if (g_issue >= (unsigned)T::STAGES) mbar_wait(empty + s, ((g_issue / T::STAGES) - 1) & 1);
+    unsigned char* st = base + (size_t)s * T::STAGE_BYTES;
+    mbar_expect_tx(full + s, T::STAGE_BYTES);
+    const int k = p_kb + p_kt * T::BK;
+    tma_load_2d(st, &tmA, k, p_m0, full + s);
+    tma_load_2d(st + T::A_BYTES, &tmB, k, p_n0, full + s);
+    ++g_issue;
+    ++p_kt;
+  };
+  if (producer)
+    for (int i = 0; i < T::STAGES - 1; ++i) issue_next();
+
+  const int wm = warp % T::WARPS_M, wn = warp / T::WARPS_M;
+  const int fr = frag_row(lane >> 2), fc = lane & 3;
+  int ktab[T::BK / 4];
+#pragma unroll
+  for (int kq = 0; kq < T::BK / 4; ++kq) ktab[kq] = swz(fr, 4 * kq + fc) - fr * 16;
+  const int abase = (wm * T::WM + fr) * 16, bbase = (wn * T::WN + fr) * 16;
+  const int c0 = frag_row(2 * fc), c1 = frag_row(2 * fc + 1);
+  unsigned gstep = 0;
+
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int m0, n0, z;
+    decode(t, m0, n0, z);
+    const int nk = ktiles_of(z);
+    double* __restrict__ C = g.C + (long long)z * g.c_zstride;
+    if (g.beta != 0.0) {   // warm L2 with this tile's C while its K loop runs
+      constexpr int LPC = (T::BM * 8 + 127) / 128;
+      for (int e = threadIdx.x; e < LPC * T::BN; e += T::THREADS) {
+        const int n = n0 + e / LPC, m = m0 + (e % LPC) * 16;
+        if (n < g.N && m < g.M)
+          asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + m + (long long)n * g.ldc));
+      }
+    }
+    double acc[T::MI][T::NI][2];
+#pragma unroll
+    for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < T::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kt = 0; kt < nk; ++kt, ++gstep) {
+      const int s = gstep % T::STAGES;
+      if (producer) issue_next();
+      mbar_wait(full + s, (gstep / T::STAGES) & 1);
+      const double* sA = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES);
+      const double* sB = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES + T::A_BYTES);
+#pragma unroll
+      for (int kq = 0; kq < T::BK / 4; ++kq) {
+        double af[T::MI], bf[T::NI];
+        const double* pa = sA + abase + ktab[kq];
+        const double* pb = sB + bbase + ktab[kq];
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i) af[i] = pa[i * 128];
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j) bf[j] = pb[j * 128];
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+    }
+    // epilogue
+    const bool use_beta = g.beta != 0.0;
+#pragma unroll
+    for (int i = 0; i < T::MI; ++i) {
+      const int m = m0 + wm * T::WM + i * 8 + fr;
+      const bool mok = m < g.M;
+      double old[T::NI][2];
+      if (use_beta) {
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int n = n0 + wn * T::WN + j * 8 + (h ? c1 : c0);
+            old[j][h] = (mok && n < g.N) ? C[m + (long long)n * g.ldc] : 0.0;
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < T::NI; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int n = n0 + wn * T::WN + j * 8 + (h ? c1 : c0);
+          if (!mok || n >= g.N) continue;
+          const double v = acc[i][j][h];
+          double out = g.alpha * v;
+          if (use_beta) out = fma(g.beta, old[j][h], out);
+          C[m + (long long)n * g.ldc] = out;
+          if (g.D2) g.D2[m + (long long)n * g.ldd2] = g.alpha2 * v;
+        }
+    }
+  }
+}
+
 }  // namespace sdc

@@ -306,6 +306,37 @@ int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B,
   return 0;
 }
 
+template <class T>
+int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
+                       const TmaGemmArgs& g, int splits) {
+  static int attr_set = 0;
+  if (!attr_set) {
+    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_persist_kernel<T>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+    attr_set = 1;
+  }
+  CUtensorMap tA, tB;
+  if (!make_tmap(&tA, A, g.K, g.M, lda, T::BM) || !make_tmap(&tB, B, g.K, g.N, ldb, T::BN)) {
+    set_err("cuTensorMapEncodeTiled failed");
+    return SDC_ERR_CUDA;
+  }
+  const long long tiles = (long long)cdiv(g.M, T::BM) * cdiv(g.N, T::BN) * splits;
+  const int grid = (int)std::min<long long>(tiles, (long long)h->num_sms * T::MINB);
+  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
+  gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, g);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
+int persist_mode() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SDC_PERSIST");
+    v = e ? atoi(e) : 1;   // 0 off, 1 short-K updates, 2 every TMA GEMM
+  }
+  return v;
+}
+
 // C = alpha A_s^T B_s + beta C  [+ D2 = alpha2 A_s^T B_s];  K-split into `splits` slices of
 // kchunk (multiple of 16) written to C + z * c_zstride when splits > 1.
 int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, long long lda,
@@ -327,6 +358,16 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
       else v = 2;
     }
     if (v == 4 && !cok) v = 0;
+    const int pm = persist_mode();
+    if (pm == 2 || (pm == 1 && v == 3)) {
+      switch (v) {
+        case 0: return launch_tma_persist<TmaL>(h, A, lda, B, ldb, g, splits);
+        case 1: return launch_tma_persist<TmaM>(h, A, lda, B, ldb, g, splits);
+        case 2: return launch_tma_persist<TmaS>(h, A, lda, B, ldb, g, splits);
+        case 3: return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
+        default: break;
+      }
+    }
     switch (v) {
       case 0: return launch_tma_t<TmaL>(h, A, lda, B, ldb, g, splits);
       case 1: return launch_tma_t<TmaM>(h, A, lda, B, ldb, g, splits);
