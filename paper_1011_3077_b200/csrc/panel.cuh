@@ -55,6 +55,34 @@ struct PanelArgs {
   int zero_above;             // rows above the panel (inside its outer WY block) to zero in Y/Y^T
 };
 
+// ---- cluster exchange by asynchronous remote stores (st.async + mbarrier tx counts) ----
+SDC_DEV uint32_t cluster_map(uint32_t local_smem_addr, int cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local_smem_addr), "r"(cta));
+  return r;
+}
+SDC_DEV void st_async_f64(uint32_t remote_addr, double v, uint32_t remote_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(remote_addr),
+               "l"(__double_as_longlong(v)), "r"(remote_mbar)
+               : "memory");
+}
+SDC_DEV void xmbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+SDC_DEV void xmbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+SDC_DEV void xmbar_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!ok);
+}
+
 // T column c of the compact-WY factor (CTA 0), from the step-c reduction results:
 //   g_i = s_i (x_i[c] + scale_c * sum_{r>c} x_i[r] x_c[r])  = Y(:,i)^T v_c   (i < c)
 //   T(0:c, c) = -tau_c T(0:c, 0:c) g,  T(c, c) = tau_c
@@ -106,6 +134,15 @@ panel_qr_kernel_t(const PanelArgs a) {
     for (int e = tid; e < PANEL_NB * PANEL_NB; e += PANEL_THREADS) Ts[e] = 0.0;
   __syncthreads();
 
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(xch + 2 * 18 * PANEL_NB);   // 2 exchange mbarriers
+  if constexpr (CLUSTER) {
+    if (tid == 0) {
+      xmbar_init(xbar, 1);
+      xmbar_init(xbar + 1, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    cooperative_groups::this_cluster().sync();   // every peer's barriers exist before any push
+  }
   const int jj = tid & (PANEL_NB - 1), rg = tid / PANEL_NB;  // column lane, row group
   const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
   unsigned long long ph[4] = {0, 0, 0, 0}, t0 = 0, t1;
@@ -115,19 +152,24 @@ panel_qr_kernel_t(const PanelArgs a) {
     // (a) partial inner products part[j] = sum_{r > k} x_r P[r][j], x = P[:,k]
     double s = 0.0;
     if (jj < nb) {
-      double s1 = 0.0;
+      // 4 rows per iteration, all 8 loads issued before the FMAs (latency-bound smem loop)
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int r = lbeg + rg;
-      for (; r + PANEL_RG < R; r += 2 * PANEL_RG) {
-        s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
-        s1 = fma(Ps[(r + PANEL_RG) * PANEL_LD + k], Ps[(r + PANEL_RG) * PANEL_LD + jj], s1);
+      for (; r + 3 * PANEL_RG < R; r += 4 * PANEL_RG) {
+        const double* q = Ps + r * PANEL_LD;
+        const double x0 = q[k], x1 = q[PANEL_RG * PANEL_LD + k], x2 = q[2 * PANEL_RG * PANEL_LD + k],
+                     x3 = q[3 * PANEL_RG * PANEL_LD + k];
+        const double p0 = q[jj], p1 = q[PANEL_RG * PANEL_LD + jj], p2 = q[2 * PANEL_RG * PANEL_LD + jj],
+                     p3 = q[3 * PANEL_RG * PANEL_LD + jj];
+        s = fma(x0, p0, s);
+        s1 = fma(x1, p1, s1);
+        s2 = fma(x2, p2, s2);
+        s3 = fma(x3, p3, s3);
       }
-      if (r < R) s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
-      s += s1;
+      for (; r < R; r += PANEL_RG) s = fma(Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj], s);
+      s = (s + s1) + (s2 + s3);
     }
     red[rg * PANEL_NB + jj] = s;
-    if (cta == tcta && k > 0)   // T column of the previous step (inputs double-buffered)
-      panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
-                     sc, tauv);
     __syncthreads();
     double* gb = a.gbuf + (size_t)(k & 1) * (G + 1) * PANEL_NB;
     double* xp = xch + (k & 1) * 18 * PANEL_NB;       // cluster mode exchange slot
@@ -141,19 +183,31 @@ panel_qr_kernel_t(const PanelArgs a) {
       }
     }
     if constexpr (CLUSTER) {
-      // push: every CTA writes its partial vector (and CTA 0 row k) into every peer's
-      // exchange slot, so after the cluster barrier all reads are local
+      // push: every CTA stores its partial vector (and CTA 0 row k) into every peer's
+      // exchange slot with st.async; each receiver's mbarrier counts the bytes, so no
+      // cluster-wide barrier is needed and all reads below are local
+      if (tid == 0)
+        xmbar_expect(xbar + (k & 1), (unsigned)(G * nb + nb) * 8u);
       __syncthreads();
-      auto cl = cooperative_groups::this_cluster();
-      if (jj < nb)
+      if (jj < nb) {
+        const double pv = red[PANEL_RG * PANEL_NB + jj];
+        const double rv = cta == 0 ? Ps[k * PANEL_LD + jj] : 0.0;
+        const uint32_t lpart = smem_u32(xp + 2 * PANEL_NB + cta * PANEL_NB + jj);
+        const uint32_t lrow = smem_u32(xp + PANEL_NB + jj);
+        const uint32_t lbar = smem_u32(xbar + (k & 1));
         for (int d = rg; d < G; d += PANEL_RG) {
-          double* dst = cl.map_shared_rank(xp, d);
-          dst[2 * PANEL_NB + cta * PANEL_NB + jj] = red[PANEL_RG * PANEL_NB + jj];
-          if (cta == 0) dst[PANEL_NB + jj] = Ps[k * PANEL_LD + jj];
+          const uint32_t rbar = cluster_map(lbar, d);
+          st_async_f64(cluster_map(lpart, d), pv, rbar);
+          if (cta == 0) st_async_f64(cluster_map(lrow, d), rv, rbar);
         }
+      }
     }
+    // T column of the previous step (inputs double-buffered), overlapping the exchange
+    if (cta == tcta && k > 0)
+      panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
+                     sc, tauv);
     if (timed) { t1 = clock64(); ph[0] += t1 - t0; t0 = t1; }
-    if constexpr (CLUSTER) cooperative_groups::this_cluster().sync();
+    if constexpr (CLUSTER) xmbar_wait(xbar + (k & 1), (k >> 1) & 1);
     else grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
     if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
     const double* row0;                                 // row k of the panel (owned by CTA 0)
@@ -205,8 +259,19 @@ panel_qr_kernel_t(const PanelArgs a) {
         // H_k applied to column jj: w = tau (P[k][jj] + scale z_jj); rows r > k: P -= w scale x_r
         const double w = tau * fma(scale, totj, drowj);
         const double ws = w * scale;
-#pragma unroll 4
-        for (int r = lbeg + rg; r < R; r += PANEL_RG)
+        int r = lbeg + rg;
+        for (; r + 3 * PANEL_RG < R; r += 4 * PANEL_RG) {   // loads first, then the stores
+          double* q = Ps + r * PANEL_LD;
+          const double x0 = q[k], x1 = q[PANEL_RG * PANEL_LD + k], x2 = q[2 * PANEL_RG * PANEL_LD + k],
+                       x3 = q[3 * PANEL_RG * PANEL_LD + k];
+          const double p0 = q[jj], p1 = q[PANEL_RG * PANEL_LD + jj], p2 = q[2 * PANEL_RG * PANEL_LD + jj],
+                       p3 = q[3 * PANEL_RG * PANEL_LD + jj];
+          q[jj] = fma(-ws, x0, p0);
+          q[PANEL_RG * PANEL_LD + jj] = fma(-ws, x1, p1);
+          q[2 * PANEL_RG * PANEL_LD + jj] = fma(-ws, x2, p2);
+          q[3 * PANEL_RG * PANEL_LD + jj] = fma(-ws, x3, p3);
+        }
+        for (; r < R; r += PANEL_RG)
           Ps[r * PANEL_LD + jj] = fma(-ws, Ps[r * PANEL_LD + k], Ps[r * PANEL_LD + jj]);
         if (cta == 0 && rg == 0) Ps[k * PANEL_LD + jj] -= w;      // diagonal row k
       }
@@ -266,7 +331,7 @@ panel_qr_kernel_t(const PanelArgs a) {
 
 inline size_t panel_smem_bytes(int rows_per) {
   return sizeof(double) * ((size_t)rows_per * PANEL_LD + (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB +
-                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB);
+                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB + 2);
 }
 
 }  // namespace sdc
