@@ -210,9 +210,13 @@ panel_qr_kernel_t(const PanelArgs a) {
     if constexpr (CLUSTER) xmbar_wait(xbar + (k & 1), (k >> 1) & 1);
     else grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
     if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
-    const double* row0;                                 // row k of the panel (owned by CTA 0)
+    // row k of the panel (owned by CTA 0): local in cluster mode; in grid mode staged into
+    // shared memory by the rg == last group during the partial-sum loads (same L2 round trip)
+    double* rows = red + PANEL_RG * PANEL_NB;          // staging row (free after the push)
+    const double* row0;
     if constexpr (CLUSTER) row0 = xp + PANEL_NB;
-    else row0 = gb + (size_t)G * PANEL_NB;
+    else row0 = rows;
+    if (!CLUSTER && rg == PANEL_RG - 1 && jj < nb) rows[jj] = __ldcg(gb + (size_t)G * PANEL_NB + jj);
     // (b) every CTA sums the per-CTA partials in the same fixed order
     if constexpr (CLUSTER) {
       double t = 0.0;
@@ -242,7 +246,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     __syncthreads();
     if (timed) { t1 = clock64(); ph[2] += t1 - t0; t0 = t1; }
     // (c) reflector of column k, computed redundantly by every thread (identical values)
-    const double alpha = CLUSTER ? row0[k] : __ldcg(row0 + k);
+    const double alpha = row0[k];
     const double sigma = sum_groups(red, k);
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (sigma != 0.0) {
@@ -253,7 +257,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     }
     if (jj < nb) {
       const double totj = sum_groups(red, jj);
-      const double drowj = CLUSTER ? row0[jj] : __ldcg(row0 + jj);
+      const double drowj = row0[jj];
       if (rg == 0) { totb[(k & 1) * PANEL_NB + jj] = totj; drowb[(k & 1) * PANEL_NB + jj] = drowj; }
       if (jj > k) {
         // H_k applied to column jj: w = tau (P[k][jj] + scale z_jj); rows r > k: P -= w scale x_r
