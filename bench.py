@@ -309,9 +309,17 @@ def main():
     p_ms, p_n, p_bytes = prof[1]
     hbm, hbm_src = hbm_peak()
     achieved = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
-    roof = {"bound": "tensor", "kernel": "gemm_dmma_kernel (all DMMA GEMM launches)",
+    traffic = None
+    try:   # DRAM bytes per launch of the representative GEMM launches, from the committed ncu capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        traffic = {k["shape"]: {"dram_bytes": k["dram_read_bytes"] + k["dram_write_bytes"],
+                                "algorithmic_bytes": k["algorithmic_bytes"]} for k in tj["kernels"]}
+        traffic["source"] = tj["source"]
+    except Exception:
+        traffic = None
+    roof = {"bound": "tensor", "kernel": "gemm_tn_tma_kernel / gemm_tn_tma_persist_kernel (all DMMA GEMM launches)",
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+            "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
             "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak_microbench.txt)",
             "share_of_step": (g_ms / prof_steps) / ms if ms > 0 else None,
             "launches_per_step": g_n // prof_steps, "timed_live": live_prof,

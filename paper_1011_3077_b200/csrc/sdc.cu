@@ -961,16 +961,16 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     ALLOC(h->AL[0], nn); ALLOC(h->AL[1], nn); ALLOC(h->BL[0], nn); ALLOC(h->BL[1], nn);
     ALLOC(h->Bh, nn); ALLOC(h->QLb, nn); ALLOC(h->VLt, nn);
   }
-  if (const char* e = getenv("SDC_NBO")) h->nbo = std::max(64, std::min(256, atoi(e) / 64 * 64));
+  if (const char* e = getenv("SDC_NBO")) h->nbo = std::max(64, std::min(512, atoi(e) / 64 * 64));
   ALLOC(h->Tb, (n / NB + 1) * NB * NB);
   ALLOC(h->Tob, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
   ALLOC(h->Tobt, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
   ALLOC(h->Zb, (size_t)h->nbo * (n + 64));
   ALLOC(h->Gb, (size_t)h->nbo * h->nbo);
   ALLOC(h->tau, n + NB);
-  h->wp_elems = (size_t)256 * (2 * (size_t)h->num_sms * 128 + 2 * n + 256);
+  h->wp_elems = (size_t)std::max(256, h->nbo) * (2 * (size_t)h->num_sms * 128 + 2 * n + 256);
   ALLOC(h->Wp, h->wp_elems);
-  ALLOC(h->W, (size_t)256 * (n + 64));
+  ALLOC(h->W, (size_t)std::max(256, h->nbo) * (n + 64));
   ALLOC(h->gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
   ALLOC(h->pmA, (n / SEL_T + 1) * n);
   if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
