@@ -49,7 +49,19 @@ enum {
   SDC_STOP_E21 = 2    /* PAPER.md:597 protocol: full split after every pass, stop at the
                          first pass whose metric <= tol (one host sync per pass)            */
 };
-enum { SDC_REGION_UNIT_DISK = 0 }; /* the only region of the step          */
+/* split regions: the step itself splits along the unit circle; the others
+ * are mapped to it before the IRS (see sdc_split_region) */
+enum {
+  SDC_REGION_UNIT_DISK = 0, /* |z| < 1                                                       */
+  SDC_REGION_DISK = 1,      /* |z| < rho (param rho > 0): unit disk of the pencil (A, rho B),
+                               the radius-rho circles of the pencil strategy */
+  SDC_REGION_HALFPLANE = 2  /* Re z < a (param a), B = I only: the line Re z = a mapped to the
+                               unit circle by f(z) = (z-a+1)/(z-a-1), i.e. the IRS runs on the
+                               pencil (A-(a-1)I, A-(a+1)I); Q^T A Q of the
+                               original A, single right subspace                             */
+};
+enum { SDC_FLAG_SYMMETRIC = 1 /* RSEP, Alg. 6: Ahat <- (Ahat + Ahat^T)/2
+                                 before the split selection; B = I only                     */ };
 enum { SDC_STATUS_SPLIT = 0, SDC_STATUS_NO_SPLIT = 1, SDC_STATUS_NONFINITE = 2 };
 #define SDC_SPLIT_ACCEPT 1e-8 /* status 0 iff metric <= this (reading Q4)       */
 
@@ -95,6 +107,17 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
               int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
               int max_iters, double tol, int stop_mode, double* Q, int ldq, double* QL, int ldql,
               double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
+
+/* The step for another split region and/or the RSEP variant (region, region_param, flags as
+ * in the enums above; all other arguments as sdc_split).  k counts the eigenvalues inside
+ * the region (|z| < rho, or Re z < a); Q(:,1:r) spans the complementary invariant subspace.
+ * Errors: -12 unknown region, -13 bad region_param, -14 unknown flag, -6 B != NULL with the
+ * half plane or the symmetric flag. */
+int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+                     int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
+                     double region_param, int flags, int max_iters, double tol, int stop_mode,
+                     double* Q, int ldq, double* QL, int ldql, double* Ahat, int ldah, double* hist,
+                     int hist_cap, sdc_result* res);
 
 /* Same step with HOST matrices (column-major, tightly packed ld = n): copies A, B, V, VL to
  * the device, runs sdc_split, and copies Q (and QL, Ahat when non-NULL) back -- the

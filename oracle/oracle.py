@@ -20,6 +20,8 @@ _lock = threading.Lock()
 _lib = None
 
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
+REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
+FLAG_SYMMETRIC = 1
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
 SPLIT_ACCEPT = 1e-8
 
@@ -51,6 +53,9 @@ def lib():
             _lib.orc_split.restype = I
             _lib.orc_split.argtypes = [I, P, I, P, I, P, I, P, I, I, D, I, P, I, P, I, P, I, P, I,
                                        ctypes.POINTER(_Result)]
+            _lib.orc_split_region.restype = I
+            _lib.orc_split_region.argtypes = [I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I,
+                                              P, I, P, I, ctypes.POINTER(_Result)]
             _lib.orc_split_select.restype = D
             _lib.orc_split_select.argtypes = [I, P, I, D, P, I, D, ctypes.POINTER(I), P]
             _lib.orc_norm1.restype = D
@@ -227,8 +232,9 @@ class SplitResult:
 
 
 def split(A, B=None, V=None, VL=None, max_iters=12, tol=0.0, stop=STOP_FIXED,
-          hist_cap=None) -> SplitResult:
-    """The whole step (RNEP if B is None, RGNEP otherwise), mirroring sdc_split."""
+          hist_cap=None, region=REGION_UNIT_DISK, param=1.0, flags=0) -> SplitResult:
+    """The whole step (RNEP if B is None, RGNEP otherwise), mirroring sdc_split /
+    sdc_split_region (region: unit disk, disk of radius param, half plane Re z < param)."""
     A = _f(A)
     n = A.shape[0]
     Bf = None if B is None else _f(B)
@@ -240,9 +246,9 @@ def split(A, B=None, V=None, VL=None, max_iters=12, tol=0.0, stop=STOP_FIXED,
     Ah = np.zeros((n, n), order="F")
     hist = np.full((hist_cap, 3), np.nan)
     res = _Result()
-    rc = lib().orc_split(n, _p(A), n, _p(Bf), n, _p(V), n, _p(VLf), n, max_iters, float(tol),
-                         int(stop), _p(Q), n, _p(QL), n, _p(Ah), n, _p(hist), hist_cap,
-                         ctypes.byref(res))
+    rc = lib().orc_split_region(n, _p(A), n, _p(Bf), n, _p(V), n, _p(VLf), n, int(region),
+                                float(param), int(flags), max_iters, float(tol), int(stop), _p(Q),
+                                n, _p(QL), n, _p(Ah), n, _p(hist), hist_cap, ctypes.byref(res))
     if rc != 0:
         raise ValueError(f"orc_split returned {rc}")
     return SplitResult(Q, QL, Ah, res.k, res.r, res.metric, res.metric_fro, res.iters,

@@ -416,11 +416,18 @@ static int all_finite(size_t cnt, const double *x) {
 static double similarity_and_select(int n, const double *A, int lda, const double *B, int ldb,
                                     const double *QR, int ldqr, const double *QLm, int ldql,
                                     double nA, double nB, double fA, double fB,
-                                    double *Ah, double *Bh, int *r, double *mfro) {
+                                    double *Ah, double *Bh, int *r, double *mfro, int sym) {
   size_t nn = (size_t)n * n;
   double *T = (double *)malloc(sizeof(double) * nn);
   orc_gemm(0, 0, n, n, n, A, lda, QR, ldqr, T, n);        /* A Q_R */
   orc_gemm(1, 0, n, n, n, QLm, ldql, T, n, Ah, n);        /* Q_L^T (A Q_R) */
+  if (sym)                                                 /* RSEP: (Ahat + Ahat^T)/2, Alg. 6 */
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < j; ++i) {
+        double v = 0.5 * (EL(Ah, i, j, n) + EL(Ah, j, i, n));
+        EL(Ah, i, j, n) = v;
+        EL(Ah, j, i, n) = v;
+      }
   if (B) {
     orc_gemm(0, 0, n, n, n, B, ldb, QR, ldqr, T, n);
     orc_gemm(1, 0, n, n, n, QLm, ldql, T, n, Bh, n);
@@ -438,11 +445,36 @@ static double similarity_and_select(int n, const double *A, int lda, const doubl
  * r* and metric are NaN unless stop_mode == ORC_STOP_E21; the R-test ratio is
  * ||R_j - R_{j-1}||_1/||R_{j-1}||_1 (NaN at j = 0) of the right IRS.
  * ---------------------------------------------------------------------------------- */
+/* Regions (the step is written for the unit disk; the others map to it):
+ *   ORC_REGION_DISK, param rho > 0: |z| < rho  <=>  unit disk of the pencil (A, rho B)
+ *     (radius-rho circles of the pencil strategy);
+ *   ORC_REGION_HALFPLANE, param a: Re z < a for B = I, via the Moebius map
+ *     f(z) = (z-a+1)/(z-a-1) that sends the line Re z = a to the unit circle:
+ *     IRS on the pencil (A-(a-1)I, A-(a+1)I); right subspace only and the
+ *     similarity Q^T A Q of the ORIGINAL A (single-matrix split, Alg. 5).
+ * Flag ORC_FLAG_SYMMETRIC (B = I only): RSEP, Ahat <- (Ahat + Ahat^T)/2 before the
+ * selection (Alg. 6). */
 int orc_split(int n, const double *A, int lda, const double *B, int ldb,
               const double *V, int ldv, const double *VL, int ldvl,
               int max_iters, double tol, int stop_mode,
               double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
               double *hist, int hist_cap, orc_result *res) {
+  return orc_split_region(n, A, lda, B, ldb, V, ldv, VL, ldvl, ORC_REGION_UNIT_DISK, 1.0, 0,
+                          max_iters, tol, stop_mode, Q, ldq, QLout, ldql, Ahat_out, ldah, hist,
+                          hist_cap, res);
+}
+
+int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
+                     const double *V, int ldv, const double *VL, int ldvl,
+                     int region, double param, int flags,
+                     int max_iters, double tol, int stop_mode,
+                     double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
+                     double *hist, int hist_cap, orc_result *res) {
+  if (region < 0 || region > 2) return -30;
+  if (region == ORC_REGION_DISK && !(param > 0.0)) return -31;
+  if ((region == ORC_REGION_HALFPLANE || (flags & ORC_FLAG_SYMMETRIC)) && B) return -32;
+  const int sym = (flags & ORC_FLAG_SYMMETRIC) != 0;
+  const double rho = region == ORC_REGION_DISK ? param : 1.0;
   if (n < 2) return -1;
   if (lda < n) return -3;
   if (B && ldb < n) return -5;
@@ -462,13 +494,18 @@ int orc_split(int n, const double *A, int lda, const double *B, int ldb,
   double *QLw = pencil ? (double *)malloc(sizeof(double) * nn) : NULL;
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) {
-      EL(Aj, i, j, n) = EL(A, i, j, lda);
-      EL(Bj, i, j, n) = pencil ? EL(B, i, j, ldb) : (i == j ? 1.0 : 0.0);
+      if (region == ORC_REGION_HALFPLANE) {           /* (A - (a-1) I, A - (a+1) I) */
+        EL(Aj, i, j, n) = EL(A, i, j, lda) - (i == j ? param - 1.0 : 0.0);
+        EL(Bj, i, j, n) = EL(A, i, j, lda) - (i == j ? param + 1.0 : 0.0);
+      } else {                                         /* (A, rho B) */
+        EL(Aj, i, j, n) = EL(A, i, j, lda);
+        EL(Bj, i, j, n) = rho * (pencil ? EL(B, i, j, ldb) : (i == j ? 1.0 : 0.0));
+      }
     }
   if (pencil) {
     Lj = (double *)malloc(sizeof(double) * nn); Mj = (double *)malloc(sizeof(double) * nn);
     for (int j = 0; j < n; ++j)
-      for (int i = 0; i < n; ++i) { EL(Lj, i, j, n) = EL(A, j, i, lda); EL(Mj, i, j, n) = EL(B, j, i, ldb); }
+      for (int i = 0; i < n; ++i) { EL(Lj, i, j, n) = EL(A, j, i, lda); EL(Mj, i, j, n) = rho * EL(B, j, i, ldb); }
   }
   double nA = orc_norm1(n, n, A, lda), fA = norm_fro(n, n, A, lda);
   double nB = pencil ? orc_norm1(n, n, B, ldb) : 1.0, fB = pencil ? norm_fro(n, n, B, ldb) : 1.0;
@@ -495,7 +532,7 @@ int orc_split(int n, const double *A, int lda, const double *B, int ldb,
       const double *QLm = Q; int ldqlm = ldq;
       if (pencil) { orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n); QLm = QLw; ldqlm = n; }
       met = similarity_and_select(n, A, lda, B, ldb, Q, ldq, QLm, ldqlm, nA, nB, fA, fB,
-                                  Ah, Bh, &r, &mfro);
+                                  Ah, Bh, &r, &mfro, sym);
       have_split = 1;
       if (hist && j < hist_cap) { hist[3 * j] = r; hist[3 * j + 1] = met; }
       if (met <= tol) { p = j + 1; conv = 1; break; }
@@ -506,7 +543,7 @@ int orc_split(int n, const double *A, int lda, const double *B, int ldb,
     const double *QLm = Q; int ldqlm = ldq;
     if (pencil) { orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n); QLm = QLw; ldqlm = n; }
     met = similarity_and_select(n, A, lda, B, ldb, Q, ldq, QLm, ldqlm, nA, nB, fA, fB,
-                                Ah, Bh, &r, &mfro);
+                                Ah, Bh, &r, &mfro, sym);
   }
   if (pencil && QLout)
     for (int j = 0; j < n; ++j)

@@ -11,6 +11,8 @@ extern "C" {
 #endif
 
 enum { ORC_STOP_FIXED = 0, ORC_STOP_RTEST = 1, ORC_STOP_E21 = 2 };
+enum { ORC_REGION_UNIT_DISK = 0, ORC_REGION_DISK = 1, ORC_REGION_HALFPLANE = 2 };
+enum { ORC_FLAG_SYMMETRIC = 1 };
 enum { ORC_STATUS_SPLIT = 0, ORC_STATUS_NO_SPLIT = 1, ORC_STATUS_NONFINITE = 2 };
 #define ORC_SPLIT_ACCEPT 1e-8 /* split_accept_tol (SPEC.md design decision; Q4) */
 
@@ -49,6 +51,13 @@ int orc_split(int n, const double *A, int lda, const double *B, int ldb,
               int max_iters, double tol, int stop_mode,
               double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
               double *hist, int hist_cap, orc_result *res);
+
+int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
+                     const double *V, int ldv, const double *VL, int ldvl,
+                     int region, double param, int flags,
+                     int max_iters, double tol, int stop_mode,
+                     double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
+                     double *hist, int hist_cap, orc_result *res);
 
 #ifdef __cplusplus
 }

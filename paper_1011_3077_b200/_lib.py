@@ -9,7 +9,8 @@ LIB_PATH = os.path.join(HERE, "libsdc.so")
 
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
-REGION_UNIT_DISK = 0
+REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
+FLAG_SYMMETRIC = 1
 PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PROF_GEMM_OTHER = 0, 1, 2, 3, 4, 5, 6
 SPLIT_ACCEPT = 1e-8
 
@@ -28,6 +29,8 @@ _SIGS = {
     "sdc_destroy": (None, [P]),
     "sdc_split": (I, [P, P, I, P, I, P, I, P, I, P, I, I, I, D, I, P, I, P, I, P, I, P, I,
                       ctypes.POINTER(SdcResult)]),
+    "sdc_split_region": (I, [P, P, I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I, P, I, P, I,
+                             ctypes.POINTER(SdcResult)]),
     "sdc_split_host": (I, [P, P, I, P, P, P, P, I, D, I, P, P, P, P, I, ctypes.POINTER(SdcResult)]),
     "sdc_dgemm": (I, [P, P, I, I, I, I, I, D, P, I, P, I, D, P, I]),
     "sdc_qr": (I, [P, P, I, I, P, I, P, I]),

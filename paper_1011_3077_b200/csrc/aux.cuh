@@ -73,6 +73,24 @@ __global__ void k_transpose_rev(double* out, long long ldo, const double* src, l
   }
 }
 
+// X(i,i) += c  (n x n)
+__global__ void k_add_diag(double* X, long long ldx, int n, double c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    X[i + (long long)i * ldx] += c;
+}
+
+// RSEP (Alg. 6): X <- (X + X^T)/2 in place; one thread per pair i < j
+__global__ void k_symmetrize(double* X, long long ldx, int n) {
+  SDC_FOR_MN(n, n) {
+    int i = (int)(_e % n), j = (int)(_e / n);
+    if (i < j) {
+      double v = 0.5 * (X[i + (long long)j * ldx] + X[j + (long long)i * ldx]);
+      X[i + (long long)j * ldx] = v;
+      X[j + (long long)i * ldx] = v;
+    }
+  }
+}
+
 // out = a + b (m x n)
 __global__ void k_add(double* out, long long ldo, const double* a, long long lda, const double* b,
                       long long ldb, int m, int n) {

@@ -88,12 +88,14 @@ struct sdc_handle {
   double *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr, *Gb = nullptr;
   // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
   struct GraphKey {
-    int n = 0, max_iters = 0, nbo = 0;
+    int n = 0, max_iters = 0, nbo = 0, region = 0, rflags = 0;
+    double rparam = 0.0;
     const void *A = nullptr, *B = nullptr, *V = nullptr, *VL = nullptr, *Q = nullptr, *QL = nullptr,
                *Ahat = nullptr;
     long long lda = 0, ldb = 0, ldv = 0, ldvl = 0, ldq = 0, ldql = 0, ldah = 0;
     bool operator==(const GraphKey& o) const {
-      return n == o.n && max_iters == o.max_iters && nbo == o.nbo && A == o.A && B == o.B && V == o.V &&
+      return n == o.n && max_iters == o.max_iters && nbo == o.nbo && region == o.region &&
+             rflags == o.rflags && rparam == o.rparam && A == o.A && B == o.B && V == o.V &&
              VL == o.VL && Q == o.Q && QL == o.QL && Ahat == o.Ahat && lda == o.lda && ldb == o.ldb &&
              ldv == o.ldv && ldvl == o.ldvl && ldq == o.ldq && ldql == o.ldql && ldah == o.ldah;
     }
@@ -104,6 +106,8 @@ struct sdc_handle {
   int graph_max_n = 4096;
   double* hscal = nullptr;             // pinned host copies of the result scalars
   const double *cur_V = nullptr, *cur_VL = nullptr;
+  int region = SDC_REGION_UNIT_DISK, rflags = 0;   // region / flags of the current call
+  double rparam = 1.0;
   long long cur_ldv = 0, cur_ldvl = 0;
   unsigned int* hflags = nullptr;      // pinned: [0] non-finite flag, [1] barrier error
   // optional per-kernel-class timing with CUDA events on the launching stream
@@ -760,6 +764,10 @@ int similarity_select(sdc_handle* h, int n, const double* A, long long lda, cons
     SDC_TRY(gemm_tn(h, n, n, n, 1.0, B, ldb, QL, ldql, 0.0, h->T1, ld));
     SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->T1, ld, Q, ldq, 0.0, h->Bh, ld));
   }
+  if (h->rflags & SDC_FLAG_SYMMETRIC) {   // RSEP (Alg. 6)
+    k_symmetrize<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->Ah, ld, n);
+    SDC_LAUNCHED(h);
+  }
   SDC_TRY(select_dev(h, n, h->Ah, ld, B ? h->Bh : nullptr, ld, h->scal, h->scal + 2, h->scal + 4));
   k_e21_fro_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(h->Ah, ld, n, h->scal + 4, h->vec);
   SDC_LAUNCHED(h);
@@ -811,17 +819,32 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
   SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
   SDC_TRY(norms(h, A, lda, n, h->scal));
   if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
-  // A_0 = A, B_0 = B (or I); stack S = [B_0; -A_0]
+  // A_0 = A, B_0 = rho B (or rho I) -- unit disk (rho = 1) or disk of radius rho;
+  // half plane Re z < a: (A_0, B_0) = (A - (a-1) I, A - (a+1) I) (Moebius map)
+  const double rho = h->region == SDC_REGION_DISK ? h->rparam : 1.0;
   k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->A[0], ld, A, lda, n, n, 1.0);
   SDC_LAUNCHED(h);
-  if (pencil) k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, 1.0);
-  else k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, 1.0);
+  if (h->region == SDC_REGION_HALFPLANE) {
+    k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, A, lda, n, n, 1.0);
+    SDC_LAUNCHED(h);
+    k_add_diag<<<cdiv(n, 256), 256, 0, h->st>>>(h->A[0], ld, n, -(h->rparam - 1.0));
+    SDC_LAUNCHED(h);
+    k_add_diag<<<cdiv(n, 256), 256, 0, h->st>>>(h->B[0], ld, n, -(h->rparam + 1.0));
+  } else if (pencil) {
+    k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, rho);
+  } else {
+    k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, rho);
+  }
   SDC_LAUNCHED(h);
   k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
   SDC_LAUNCHED(h);
   if (pencil) {   // left IRS on (A^T, B^T)
     SDC_TRY(transpose_rev(h, h->AL[0], ld, A, lda, n, 0));
     SDC_TRY(transpose_rev(h, h->BL[0], ld, B, ldb, n, 0));
+    if (rho != 1.0) {
+      k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->BL[0], ld, h->BL[0], ld, n, n, rho);
+      SDC_LAUNCHED(h);
+    }
     k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->SL, m, h->AL[0], ld, h->BL[0], ld, n);
     SDC_LAUNCHED(h);
   }
@@ -1029,7 +1052,28 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
               int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
               int max_iters, double tol, int stop_mode, double* Q, int ldq, double* QL, int ldql,
               double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res) {
+  if (region != SDC_REGION_UNIT_DISK) { set_err("sdc_split: use sdc_split_region for region %d", region); return -12; }
+  return sdc_split_region(h, stream, n, A, lda, B, ldb, V, ldv, VL, ldvl, region, 1.0, 0, max_iters,
+                          tol, stop_mode, Q, ldq, QL, ldql, Ahat, ldah, hist, hist_cap, res);
+}
+
+int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
+                     int ldb, const double* V, int ldv, const double* VL, int ldvl, int region,
+                     double region_param, int flags, int max_iters, double tol, int stop_mode,
+                     double* Q, int ldq, double* QL, int ldql, double* Ahat, int ldah, double* hist,
+                     int hist_cap, sdc_result* res) {
   SDC_TRY(check_handle(h));
+  if (region < 0 || region > 2) { set_err("unknown region %d", region); return -12; }
+  if (region == SDC_REGION_DISK && !(region_param > 0.0)) { set_err("disk radius must be > 0"); return -13; }
+  if (region == SDC_REGION_HALFPLANE && !std::isfinite(region_param)) { set_err("bad half-plane abscissa"); return -13; }
+  if ((region == SDC_REGION_HALFPLANE || (flags & SDC_FLAG_SYMMETRIC)) && B) {
+    set_err("half-plane regions and the symmetric flag take B = NULL (B = I)");
+    return -6;
+  }
+  if (flags & ~SDC_FLAG_SYMMETRIC) { set_err("unknown flags"); return -14; }
+  h->region = region;
+  h->rparam = region == SDC_REGION_UNIT_DISK ? 1.0 : region_param;
+  h->rflags = flags;
   if (n < 2 || n > h->n_max) { set_err("n=%d outside [2, n_max=%d]", n, h->n_max); return -3; }
   if (!A) { set_err("A is NULL"); return -4; }
   if (lda < n) { set_err("lda < n"); return -5; }
@@ -1040,7 +1084,6 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
   if (ldv < n) { set_err("ldv < n"); return -9; }
   if (pencil && !VL) { set_err("VL is NULL for a pencil"); return -10; }
   if (pencil && ldvl < n) { set_err("ldvl < n"); return -11; }
-  if (region != SDC_REGION_UNIT_DISK) { set_err("unknown region %d", region); return -12; }
   if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -13; }
   if (!(tol >= 0.0)) { set_err("tol < 0"); return -14; }
   if (stop_mode < 0 || stop_mode > 2) { set_err("unknown stop mode"); return -15; }
@@ -1064,6 +1107,7 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
     // and replayed while the call signature is unchanged
     sdc_handle::GraphKey key;
     key.n = n; key.max_iters = max_iters; key.nbo = h->nbo;
+    key.region = h->region; key.rflags = h->rflags; key.rparam = h->rparam;
     key.A = A; key.B = B; key.V = V; key.VL = VL; key.Q = Q; key.QL = QL; key.Ahat = Ahat;
     key.lda = lda; key.ldb = ldb; key.ldv = ldv; key.ldvl = ldvl; key.ldq = ldq; key.ldql = ldql;
     key.ldah = ldah;

@@ -172,3 +172,83 @@ def make_config(cfg: int, n: int | None = None, device=None) -> Problem:
         return Problem("cfg5", n, A, None, V, None, 30, 0.0, STOP_FIXED,
                        expected_k=int(np.sum(eig < 1)))
     raise ValueError(cfg)
+
+
+# ---------------------------------------------------------------------------------------
+# the paper's numerical experiments (Figures numexp_rand / numexp_hard):
+# normal matrices with random eigenvalues under a random orthogonal similarity, split on
+# the imaginary axis (half plane Re z < 0).  Real matrices: complex eigenvalues come in
+# conjugate pairs, realised as 2x2 blocks [[x, y], [-y, x]] (eigenvalues x +- i y).
+# ---------------------------------------------------------------------------------------
+def _pairs_block(xs, ys):
+    m = len(xs)
+    D = np.zeros((2 * m, 2 * m))
+    for t, (x, y) in enumerate(zip(xs, ys)):
+        D[2 * t, 2 * t] = D[2 * t + 1, 2 * t + 1] = x
+        D[2 * t, 2 * t + 1] = y
+        D[2 * t + 1, 2 * t] = -y
+    return D
+
+
+def normal_random_eigs(n: int, seed: int, vseed: int, lo: float = -1.5, hi: float = 1.5):
+    """E1/E2 (PAPER.md:599): Re, Im ~ U[lo, hi] (n//2 conjugate pairs, one real eigenvalue
+    if n is odd), A = U D U^T with U Haar.  Returns (A, V, eigenvalues)."""
+    g = np.random.default_rng(seed)
+    m = n // 2
+    xs, ys = g.uniform(lo, hi, m), g.uniform(lo, hi, m)
+    D = np.zeros((n, n))
+    D[:2 * m, :2 * m] = _pairs_block(xs, ys)
+    eig = list(xs + 1j * ys) + list(xs - 1j * ys)
+    if n % 2:
+        x0 = g.uniform(lo, hi)
+        D[n - 1, n - 1] = x0
+        eig.append(x0)
+    U = haar(g.standard_normal((n, n)))
+    A = U @ D @ U.T
+    V = haar(np.random.default_rng(vseed).standard_normal((n, n)))
+    return _finish(A, None), _finish(V, None), np.array(eig)
+
+
+def imag_axis_eigs(n: int, seed: int, vseed: int, eps: float = 1e-10):
+    """E3: Re lambda = +-eps (random signs), Im ~ U[-1.5, 1.5], orthogonal
+    eigenvectors."""
+    g = np.random.default_rng(seed)
+    m = n // 2
+    xs = eps * np.where(g.uniform(size=m) < 0.5, -1.0, 1.0)
+    ys = g.uniform(-1.5, 1.5, m)
+    D = np.zeros((n, n))
+    D[:2 * m, :2 * m] = _pairs_block(xs, ys)
+    eig = list(xs + 1j * ys) + list(xs - 1j * ys)
+    if n % 2:
+        x0 = eps * (1.0 if g.uniform() < 0.5 else -1.0)
+        D[n - 1, n - 1] = x0
+        eig.append(x0)
+    U = haar(g.standard_normal((n, n)))
+    V = haar(np.random.default_rng(vseed).standard_normal((n, n)))
+    return _finish(U @ D @ U.T, None), _finish(V, None), np.array(eig)
+
+
+def jordan_case(n: int, seed: int, vseed: int, mu: float = 0.1):
+    """E4: n/2 random eigenvalues with negative real part (Re ~ U[-1.5, 0),
+    Im ~ U[-1.5, 1.5], conjugate pairs) and one n/2 x n/2 Jordan block at mu, under a random
+    orthogonal similarity (non-normal; the imaginary axis meets its pseudospectrum)."""
+    g = np.random.default_rng(seed)
+    h = n // 2
+    m = h // 2
+    xs, ys = g.uniform(-1.5, 0.0, m), g.uniform(-1.5, 1.5, m)
+    D = np.zeros((n, n))
+    D[:2 * m, :2 * m] = _pairs_block(xs, ys)
+    J = mu * np.eye(n - h) + np.diag(np.ones(n - h - 1), 1)
+    D[h:, h:] = J
+    U = haar(g.standard_normal((n, n)))
+    V = haar(np.random.default_rng(vseed).standard_normal((n, n)))
+    eig = np.array(list(xs + 1j * ys) + list(xs - 1j * ys) + [mu] * (n - h))
+    return _finish(U @ D @ U.T, None), _finish(V, None), eig
+
+
+EXPERIMENTS = {   # PAPER.md:597-603
+    "E1": dict(fn=normal_random_eigs, n=100, seed=101, vseed=1101, passes=60),
+    "E2": dict(fn=normal_random_eigs, n=1000, seed=102, vseed=1102, passes=60),
+    "E3": dict(fn=imag_axis_eigs, n=25, seed=103, vseed=1103, passes=60),
+    "E4": dict(fn=jordan_case, n=32, seed=104, vseed=1104, passes=60),
+}

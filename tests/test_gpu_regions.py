@@ -1,0 +1,72 @@
+"""GPU parity (-m gpu) of the other split regions and the RSEP flag against the oracle:
+k, r exact; principal angle of span Q(:,1:r) <= 1e-9; |metric difference| <= 1e-12;
+||Q^T Q - I||_F <= 1e-13 n (north_star criteria)."""
+import numpy as np
+import pytest
+import torch
+
+from _util import orth_err, sin_angle
+from paper_1011_3077_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def handle():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1011_3077_b200 import api
+    return api.Handle(1024)
+
+
+def dev(x):
+    return torch.as_tensor(np.asfortranarray(x), dtype=torch.float64).cuda().t().contiguous().t()
+
+
+def check(o, Q, info, n):
+    assert (info.k, info.r) == (o.k, o.r)
+    assert abs(info.metric - o.metric) <= 1e-12
+    q = Q.cpu().numpy()
+    assert orth_err(q) <= 1e-13 * n
+    assert sin_angle(q[:, :info.r], o.Q[:, :o.r]) <= 1e-9
+
+
+@pytest.mark.parametrize("n,a", [(100, 0.0), (257, 0.25)])
+def test_halfplane_parity(orc, handle, n, a):
+    A, V, eig = inputs.normal_random_eigs(n, 900 + n, 1900 + n)
+    Q, _, _, info = handle.split(dev(A), None, dev(V), max_iters=40, region="halfplane", param=a)
+    o = orc.split(A, V=V, max_iters=40, region=orc.REGION_HALFPLANE, param=a)
+    check(o, Q, info, n)
+    assert info.k == int(np.sum(eig.real < a))
+
+
+def test_disk_parity(orc, handle):
+    n, rho = 200, 0.9
+    A, V = inputs.ginibre(n, 21, 1021)
+    Q, _, _, info = handle.split(dev(A), None, dev(V), max_iters=30, region="disk", param=rho)
+    o = orc.split(A, V=V, max_iters=30, region=orc.REGION_DISK, param=rho)
+    check(o, Q, info, n)
+
+
+def test_rsep_parity(orc, handle):
+    n = 300
+    g = np.random.default_rng(31)
+    lam = np.concatenate([g.uniform(-0.85, 0.85, 150), g.uniform(1.15, 2.5, 75), -g.uniform(1.15, 2.5, 75)])
+    U = inputs.haar(g.standard_normal((n, n)))
+    A = (U * lam) @ U.T
+    A = (A + A.T) / 2
+    V = inputs.haar(g.standard_normal((n, n)))
+    Q, _, Ah, info = handle.split(dev(A), None, dev(V), max_iters=20, symmetric=True, want_ahat=True)
+    o = orc.split(A, V=V, max_iters=20, flags=orc.FLAG_SYMMETRIC)
+    check(o, Q, info, n)
+    ah = Ah.cpu().numpy()
+    assert np.array_equal(ah, ah.T) and info.k == 150
+
+
+def test_region_argument_errors(handle):
+    from paper_1011_3077_b200._lib import SdcError
+    A = dev(2 * np.eye(8))
+    with pytest.raises(SdcError):
+        handle.split(A, dev(np.eye(8)), dev(np.eye(8)), dev(np.eye(8)), region="halfplane")
+    with pytest.raises(SdcError):
+        handle.split(A, None, dev(np.eye(8)), region="disk", param=-1.0)
