@@ -70,3 +70,34 @@ def test_region_argument_errors(handle):
         handle.split(A, dev(np.eye(8)), dev(np.eye(8)), dev(np.eye(8)), region="halfplane")
     with pytest.raises(SdcError):
         handle.split(A, None, dev(np.eye(8)), region="disk", param=-1.0)
+
+
+def _monitor(handle, name):
+    e = inputs.EXPERIMENTS[name]
+    A, V, eig = e["fn"](e["n"], e["seed"], e["vseed"])
+    _, _, _, info = handle.split(dev(A), None, dev(V), max_iters=e["passes"], tol=0.0, stop="e21",
+                                 region="halfplane", param=0.0)
+    return info, info.hist[:, 1], eig
+
+
+def _first_at_floor(hist):
+    floor = np.min(hist)
+    return 1 + int(np.argmax(hist <= 100 * floor))
+
+
+def test_paper_experiments_landmarks(handle):
+    # PAPER.md:599-603 (E1-E4), split on the imaginary axis, full split after every pass:
+    # E1/E2 (normal, random eigenvalues, n=100 / 1000) converge at about the same pass;
+    # E3 (Re lambda = +-1e-10, n=25) converges within 40 passes; E4 (16x16 Jordan block at
+    # 0.1 next to the axis) does not converge in 60 passes.
+    i1, h1, e1 = _monitor(handle, "E1")
+    i2, h2, e2 = _monitor(handle, "E2")
+    i3, h3, e3 = _monitor(handle, "E3")
+    i4, h4, _ = _monitor(handle, "E4")
+    for info, hist, eig in ((i1, h1, e1), (i2, h2, e2), (i3, h3, e3)):
+        assert info.k == int(np.sum(eig.real < 0)) and info.status == 0
+        assert np.min(hist) <= 1e-10
+    p1, p2, p3 = _first_at_floor(h1), _first_at_floor(h2), _first_at_floor(h3)
+    assert abs(p1 - p2) <= 6 and max(p1, p2) <= 20
+    assert p3 <= 40 and np.all(h3[:30] > 1e-3)
+    assert i4.status == 1 and np.min(h4[20:]) > 1e-6
