@@ -69,6 +69,24 @@ SDC_DEV void grid_barrier(unsigned int* ctr, unsigned int target) {
   __syncthreads();
 }
 
+// Barrier where only `arrive` CTAs (cluster leaders) add to the counter but every CTA waits
+// for the target; bounded spin as grid_barrier.
+SDC_DEV void leaders_barrier(unsigned int* ctr, unsigned int target, bool arrive) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (arrive) red_release_gpu_add(ctr, 1u);
+    unsigned int polls = 0;
+    while (ld_acquire_gpu(ctr) < target) {
+      if (++polls > (1u << 26)) {
+        atomicExch(ctr + 1, 1u);
+        break;
+      }
+      if (polls > 64) __nanosleep(32);
+    }
+  }
+  __syncthreads();
+}
+
 SDC_DEV double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

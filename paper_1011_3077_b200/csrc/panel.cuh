@@ -53,6 +53,7 @@ struct PanelArgs {
   int rows_per;               // rows owned per CTA (CTA 0 owns rows [0, rows_per) >= nb)
   unsigned long long* dbg;    // optional phase timers (CTA 0 / last CTA, thread 0), or null
   int zero_above;             // rows above the panel (inside its outer WY block) to zero in Y/Y^T
+  int csize;                  // cluster mode: CTAs per cluster (G / csize clusters)
 };
 
 // ---- cluster exchange by asynchronous remote stores (st.async + mbarrier tx counts) ----
@@ -182,23 +183,26 @@ panel_qr_kernel_t(const PanelArgs a) {
         if (cta == 0) __stcg(gb + (size_t)G * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);  // row k
       }
     }
+    const int CS = CLUSTER ? a.csize : 1;               // CTAs per cluster
+    const int NCL = CLUSTER ? G / CS : 1;               // clusters (> 1: two-level exchange)
+    const int crank = cta % CS, cid = cta / CS;
     if constexpr (CLUSTER) {
-      // push: every CTA stores its partial vector (and CTA 0 row k) into every peer's
-      // exchange slot with st.async; each receiver's mbarrier counts the bytes, so no
-      // cluster-wide barrier is needed and all reads below are local
+      // push: every CTA stores its partial vector (and, single-cluster, CTA 0 row k) into
+      // every peer's exchange slot with st.async; each receiver's mbarrier counts the
+      // bytes, so no cluster-wide barrier is needed and all reads below are local
       if (tid == 0)
-        xmbar_expect(xbar + (k & 1), (unsigned)(G * nb + nb) * 8u);
+        xmbar_expect(xbar + (k & 1), (unsigned)(CS * nb + (NCL == 1 ? nb : 0)) * 8u);
       __syncthreads();
       if (jj < nb) {
         const double pv = red[PANEL_RG * PANEL_NB + jj];
         const double rv = cta == 0 ? Ps[k * PANEL_LD + jj] : 0.0;
-        const uint32_t lpart = smem_u32(xp + 2 * PANEL_NB + cta * PANEL_NB + jj);
+        const uint32_t lpart = smem_u32(xp + 2 * PANEL_NB + crank * PANEL_NB + jj);
         const uint32_t lrow = smem_u32(xp + PANEL_NB + jj);
         const uint32_t lbar = smem_u32(xbar + (k & 1));
-        for (int d = rg; d < G; d += PANEL_RG) {
+        for (int d = rg; d < CS; d += PANEL_RG) {
           const uint32_t rbar = cluster_map(lbar, d);
           st_async_f64(cluster_map(lpart, d), pv, rbar);
-          if (cta == 0) st_async_f64(cluster_map(lrow, d), rv, rbar);
+          if (cta == 0 && NCL == 1) st_async_f64(cluster_map(lrow, d), rv, rbar);
         }
       }
     }
@@ -207,18 +211,51 @@ panel_qr_kernel_t(const PanelArgs a) {
       panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
                      sc, tauv);
     if (timed) { t1 = clock64(); ph[0] += t1 - t0; t0 = t1; }
-    if constexpr (CLUSTER) xmbar_wait(xbar + (k & 1), (k >> 1) & 1);
-    else grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
+    if constexpr (CLUSTER) {
+      xmbar_wait(xbar + (k & 1), (k >> 1) & 1);
+      if (NCL > 1) {
+        // two-level: every CTA forms its cluster's sum (same fixed order); the leaders
+        // publish them (and CTA 0 row k) through L2; one counter arrival per cluster
+        double t = 0.0;
+        if (jj < nb) {
+#pragma unroll
+          for (int u = 0; u < 16 / PANEL_RG; ++u) {
+            const int c = rg + PANEL_RG * u;
+            t += c < CS ? xp[2 * PANEL_NB + c * PANEL_NB + jj] : 0.0;
+          }
+        }
+        red[rg * PANEL_NB + jj] = t;
+        __syncthreads();
+        if (tid < nb && crank == 0) {
+          __stcg(gb + (size_t)cid * PANEL_NB + tid, sum_groups(red, tid));
+          if (cta == 0) __stcg(gb + (size_t)NCL * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);
+        }
+        leaders_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)NCL, crank == 0);
+      }
+    } else {
+      grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
+    }
     if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
     // row k of the panel (owned by CTA 0): local in cluster mode; in grid mode staged into
     // shared memory by the rg == last group during the partial-sum loads (same L2 round trip)
     double* rows = red + PANEL_RG * PANEL_NB;          // staging row (free after the push)
     const double* row0;
-    if constexpr (CLUSTER) row0 = xp + PANEL_NB;
+    if (CLUSTER && NCL == 1) row0 = xp + PANEL_NB;
     else row0 = rows;
-    if (!CLUSTER && rg == PANEL_RG - 1 && jj < nb) rows[jj] = __ldcg(gb + (size_t)G * PANEL_NB + jj);
-    // (b) every CTA sums the per-CTA partials in the same fixed order
-    if constexpr (CLUSTER) {
+    if ((!CLUSTER || NCL > 1) && rg == PANEL_RG - 1 && jj < nb)
+      rows[jj] = __ldcg(gb + (size_t)(CLUSTER ? NCL : G) * PANEL_NB + jj);
+    // (b) every CTA sums the per-CTA (per-cluster) partials in the same fixed order
+    if (CLUSTER && NCL > 1) {
+      double t = 0.0;
+      if (jj < nb) {
+#pragma unroll
+        for (int u = 0; u < 16 / PANEL_RG; ++u) {
+          const int c = rg + PANEL_RG * u;
+          t += c < NCL ? __ldcg(gb + (size_t)c * PANEL_NB + jj) : 0.0;
+        }
+      }
+      red[rg * PANEL_NB + jj] = t;
+    } else if constexpr (CLUSTER) {
       double t = 0.0;
       if (jj < nb) {
 #pragma unroll

@@ -83,6 +83,8 @@ struct sdc_handle {
   bool dbg_on = false;
   int panel_rows = 128;                // target rows per panel CTA
   bool cluster_ok = false;             // 16-CTA clusters usable for the panel kernel
+  bool mcluster_ok = false;            // several co-resident 16-CTA clusters (tall panels)
+  int max_clusters16 = 0;
   int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width (multiple of 64)
   double *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr, *Gb = nullptr;
@@ -463,15 +465,32 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
 // ---------------------------------------------------------------------------------------
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
-  // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange), else a cooperative grid
-  const bool cluster = h->cluster_ok && m <= h->cluster_max_rows;
-  int G = cluster ? std::min(16, std::max(1, cdiv(m, h->panel_rows)))
-                  : std::min(h->num_sms, std::max(1, m / h->panel_rows));
+  // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange); taller panels: several
+  // 16-CTA clusters with a two-level exchange (DSMEM inside, L2 between cluster leaders);
+  // otherwise a cooperative grid exchanging through L2
+  bool cluster = h->cluster_ok && m <= h->cluster_max_rows;
+  int csize = 1, G;
+  if (cluster) {
+    G = std::min(16, std::max(1, cdiv(m, h->panel_rows)));
+  } else if (h->mcluster_ok) {
+    const int ncl = std::max(2, std::min(h->max_clusters16, cdiv(m, 16 * h->panel_rows)));
+    if (panel_smem_bytes(cdiv(m, 16 * ncl)) <= 227 * 1024) {
+      cluster = true;
+      csize = 16;
+      G = 16 * ncl;
+    } else {
+      G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
+    }
+  } else {
+    G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
+  }
   int rows_per = cdiv(m, G);
   if (rows_per < nb) {
     rows_per = nb;
     G = cdiv(m, rows_per);
+    if (csize > 1) { cluster = false; csize = 1; G = std::min(G, h->num_sms); rows_per = cdiv(m, G); }
   }
+  if (cluster && csize == 1) csize = G;
   size_t smem = panel_smem_bytes(rows_per);
   static size_t attr_smem[2] = {0, 0};
   if (smem > attr_smem[cluster]) {
@@ -485,7 +504,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     attr_smem[cluster] = smem;
   }
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
-              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above};
+              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   if (cluster) {
     cudaLaunchConfig_t cfg = {};
@@ -495,12 +514,13 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     cfg.stream = h->st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = G;
+    attr[0].val.clusterDim.x = csize;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     SDC_CK(cudaLaunchKernelEx(&cfg, panel_qr_kernel_t<true>, a));
+    if (G > csize) h->bar_count += (unsigned long long)(G / csize) * nb;
   } else {
     void* args[] = {&a};
     SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel_t<false>, dim3(G),
@@ -1036,9 +1056,19 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
       int ncl = 0;
       if (cudaOccupancyMaxActiveClusters(&ncl, panel_qr_kernel_t<true>, &cfg) == cudaSuccess && ncl >= 1)
         h->cluster_ok = true;
+      // tall panels: how many 16-CTA clusters with ~256-row blocks can be resident at once
+      cfg.dynamicSmemBytes = panel_smem_bytes(256);
+      cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)panel_smem_bytes(256));
+      int ncl2 = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl2, panel_qr_kernel_t<true>, &cfg) == cudaSuccess && ncl2 >= 2) {
+        h->max_clusters16 = ncl2;
+        h->mcluster_ok = true;
+      }
       cudaGetLastError();
     }
-    if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = false;
+    if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = h->mcluster_ok = false;
+    if (getenv("SDC_NO_MCLUSTER")) h->mcluster_ok = false;
   }
   if (!rc && cudaMallocHost(&h->hscal, sizeof(double) * (SCAL_HIST + MAX_HIST)) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
