@@ -31,7 +31,8 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp", SRC]
+        extra = os.environ.get("SDC_NVCC_EXTRA", "").split()   # e.g. -DSDC_PANEL_SUBPHASES (dev)
+        cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB + ".tmp", SRC]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
     return LIB

@@ -31,14 +31,34 @@ constexpr int PANEL_NB = 64;        // max panel width
 constexpr int PANEL_THREADS = 512;
 constexpr int PANEL_RG = PANEL_THREADS / PANEL_NB;   // row groups (8)
 
+// fixed-order pairwise sum of 16 values
+SDC_DEV double tree16(const double* v) {
+  return (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) +
+         (((v[8] + v[9]) + (v[10] + v[11])) + ((v[12] + v[13]) + (v[14] + v[15])));
+}
+// fixed-order sum of the first n (<= 16) exchange slots x[c * PANEL_NB]
+SDC_DEV double sum_slots(const double* x, int n) {
+  double v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v[c] = c < n ? x[c * 64] : 0.0;
+  return tree16(v);
+}
+
 // fixed-order sum of the PANEL_RG row-group partials of column j
 SDC_DEV double sum_groups(const double* red, int j) {
-  double t = 0.0;
-#pragma unroll
-  for (int g = 0; g < PANEL_RG; ++g) t += red[g * 64 + j];
-  return t;
+  static_assert(PANEL_RG == 8, "tree below");
+  const double* r = red + j;
+  return ((r[0] + r[64]) + (r[128] + r[192])) + ((r[256] + r[320]) + (r[384] + r[448]));
 }
-constexpr int PANEL_LD = PANEL_NB + 1;  // smem row stride (doubles) of the local panel
+constexpr int PANEL_LD = PANEL_NB + 1;
+
+// (q == i) computed opaquely, so that per-element selects on a register array are not
+// folded into a dynamically indexed (local-memory) access
+SDC_DEV bool sel_bit(int q, int i) {
+  unsigned r;
+  asm("{\n .reg .pred p;\n setp.eq.s32 p, %1, %2;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(r) : "r"(q), "r"(i));
+  return r != 0;
+}  // smem row stride (doubles) of the local panel
 
 struct PanelArgs {
   double* P; long long ldp;   // panel (m x nb), factored in place (R upper, v below)
@@ -54,7 +74,26 @@ struct PanelArgs {
   unsigned long long* dbg;    // optional phase timers (CTA 0 / last CTA, thread 0), or null
   int zero_above;             // rows above the panel (inside its outer WY block) to zero in Y/Y^T
   int csize;                  // cluster mode: CTAs per cluster (G / csize clusters)
+  double* ll;                 // multi-cluster: flag-carrying slots, 2 x (16 + 1) x PANEL_NB x 16 B
+  unsigned epoch;             // multi-cluster: flag of column k is epoch + k + 1 (unique per call)
 };
+constexpr size_t PANEL_LL_DOUBLES = 2 * 17 * 64 * 2;
+
+// "LL" exchange through L2: a double travels as two 8-byte words {flag:32 | half:32}; each
+// word is single-copy atomic, so a reader that sees both flags sees the value -- no fence,
+// no separate counter (one L2 round trip instead of release + counter + acquire + load).
+SDC_DEV void ll_store(double* slot, double v, unsigned flag) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long w0 = ((unsigned long long)flag << 32) | (b & 0xffffffffull);
+  const unsigned long long w1 = ((unsigned long long)flag << 32) | (b >> 32);
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(slot), "l"(w0), "l"(w1) : "memory");
+}
+SDC_DEV bool ll_load(const double* slot, unsigned flag, double& v) {
+  unsigned long long w0, w1;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(w0), "=l"(w1) : "l"(slot) : "memory");
+  v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+  return (unsigned)(w0 >> 32) == flag && (unsigned)(w1 >> 32) == flag;
+}
 
 // ---- cluster exchange by asynchronous remote stores (st.async + mbarrier tx counts) ----
 SDC_DEV uint32_t cluster_map(uint32_t local_smem_addr, int cta) {
@@ -78,7 +117,7 @@ SDC_DEV void xmbar_wait(uint64_t* bar, unsigned parity) {
   uint32_t ok;
   do {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   } while (!ok);
@@ -107,16 +146,28 @@ SDC_DEV void panel_t_column(double* Ts, int c, const double* tot, const double* 
 // CLUSTER = true : the G <= 16 CTAs form ONE thread-block cluster and exchange partials
 //                  through distributed shared memory with a cluster barrier (~0.2 us instead
 //                  of ~1-2 us per column; used when the panel fits in 16 SMs' shared memory).
-template <bool CLUSTER>
+//
+// RPT > 0: the column loop runs out of REGISTERS: thread (jj, rg) holds rows rg + 8i
+// (i < RPT) of column jj, so the partial products and the rank-1 update are register FMAs;
+// only the reflector column x_k (zeroed at rows <= k, staged by its owner thread during the
+// previous update) and row k (CTA 0) pass through shared memory.  RPT = 0: the panel
+// stays in shared memory (any rows_per).  Shared memory still stages the coalesced
+// load / write-back of the row block.
+template <bool CLUSTER, int RPT>
 __global__ void __launch_bounds__(PANEL_THREADS)
 panel_qr_kernel_t(const PanelArgs a) {
   extern __shared__ __align__(16) double sm[];
+  const unsigned long long tstart = clock64();
+  constexpr bool REG = RPT > 0;
+  constexpr int XS = REG ? PANEL_RG * RPT : 0;      // one staged column (by owner layout)
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
   const int nb = a.nb;
   const int r0 = cta * a.rows_per;
   const int r1 = min(a.m, r0 + a.rows_per);
   const int R = max(0, r1 - r0);
-  double* Ps = sm;                                  // R x PANEL_LD, row-major local block
+  double* xs = sm;                                  // REG: 2 x XS staged column x_k (parity)
+  double* rowst = sm + 2 * XS;                      // REG: row k of the panel (CTA 0)
+  double* Ps = rowst + (REG ? PANEL_NB : 0);        // R x PANEL_LD, row-major local block
   double* red = Ps + (size_t)a.rows_per * PANEL_LD; // PANEL_RG x PANEL_NB
   double* totb = red + (PANEL_RG + 1) * PANEL_NB;                // 2 x PANEL_NB (by column parity)
   double* drowb = totb + 2 * PANEL_NB;              // 2 x PANEL_NB
@@ -126,10 +177,13 @@ panel_qr_kernel_t(const PanelArgs a) {
   double* xch = Ts + PANEL_NB * PANEL_NB;           // cluster mode: 2 x {-, row k, 16 partials}
 
   // load the CTA's row block
+  // all loads in flight at once (cp.async), one HBM round trip instead of R*nb/threads
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {
     int j = e / R, r = e % R;                       // coalesced along rows
-    Ps[r * PANEL_LD + j] = a.P[(long long)(r0 + r) + (long long)j * a.ldp];
+    cp_async_zfill<8>(Ps + r * PANEL_LD + j, a.P + (long long)(r0 + r) + (long long)j * a.ldp, 8);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   const int tcta = G - 1;                          // builds T (fewest rows: off the critical path)
   if (cta == tcta)
     for (int e = tid; e < PANEL_NB * PANEL_NB; e += PANEL_THREADS) Ts[e] = 0.0;
@@ -145,14 +199,54 @@ panel_qr_kernel_t(const PanelArgs a) {
     cooperative_groups::this_cluster().sync();   // every peer's barriers exist before any push
   }
   const int jj = tid & (PANEL_NB - 1), rg = tid / PANEL_NB;  // column lane, row group
+  double p[REG ? RPT : 1];                          // REG: rows rg + 8i of column jj
+  if constexpr (REG) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = rg + PANEL_RG * i;
+      p[i] = (r < R && jj < nb) ? Ps[r * PANEL_LD + jj] : 0.0;
+    }
+    if (jj == 0) {                                  // stage x_0 (rows > 0)
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) xs[rg * RPT + i] = r0 + rg + PANEL_RG * i > 0 ? p[i] : 0.0;
+    }
+    if (cta == 0 && rg == 0) rowst[jj] = p[0];     // row 0
+    __syncthreads();
+  }
+  const int CS = CLUSTER ? a.csize : 1;               // CTAs per cluster
+  const int NCL = CLUSTER ? G / CS : 1;               // clusters (> 1: two-level exchange)
+  const int crank = cta % CS, cid = cta / CS;
   const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
   unsigned long long ph[4] = {0, 0, 0, 0}, t0 = 0, t1;
+#ifdef SDC_PANEL_SUBPHASES   // fine-grained phase timers (tools/panel_bench.py; costs registers)
+  unsigned long long sp[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tsp = 0;
+#define PSTAMP(q) if (timed) { const unsigned long long _t = clock64(); sp[q] += _t - tsp; tsp = _t; }
+#define PSTAMP0() if (timed) tsp = t0
+#else
+#define PSTAMP(q)
+#define PSTAMP0()
+#endif
+  const unsigned long long tloop = clock64();
   for (int k = 0; k < nb; ++k) {
     if (timed) t0 = clock64();
+    PSTAMP0();
     const int lbeg = max(0, k + 1 - r0);               // local rows with global index > k
     // (a) partial inner products part[j] = sum_{r > k} x_r P[r][j], x = P[:,k]
     double s = 0.0;
-    if (jj < nb) {
+    const double* xk = xs + (k & 1) * XS + rg * RPT;   // REG: x_k at this thread's rows
+    if constexpr (REG) {
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < RPT; i += 4) {
+        const double2 u = *reinterpret_cast<const double2*>(xk + i);
+        const double2 v = *reinterpret_cast<const double2*>(xk + i + 2);
+        s = fma(u.x, p[i], s);
+        s1 = fma(u.y, p[i + 1], s1);
+        s2 = fma(v.x, p[i + 2], s2);
+        s3 = fma(v.y, p[i + 3], s3);
+      }
+      s = (s + s1) + (s2 + s3);
+    } else if (jj < nb) {
       // 4 rows per iteration, all 8 loads issued before the FMAs (latency-bound smem loop)
       double s1 = 0.0, s2 = 0.0, s3 = 0.0;
       int r = lbeg + rg;
@@ -171,21 +265,20 @@ panel_qr_kernel_t(const PanelArgs a) {
       s = (s + s1) + (s2 + s3);
     }
     red[rg * PANEL_NB + jj] = s;
+    PSTAMP(0);
     __syncthreads();
     double* gb = a.gbuf + (size_t)(k & 1) * (G + 1) * PANEL_NB;
     double* xp = xch + (k & 1) * 18 * PANEL_NB;       // cluster mode exchange slot
     if (tid < nb) {
-      double p = sum_groups(red, tid);
+      const double pv = sum_groups(red, tid);
       if constexpr (CLUSTER) {
-        red[PANEL_RG * PANEL_NB + tid] = p;       // staged for the push below
+        red[PANEL_RG * PANEL_NB + tid] = pv;      // staged for the push below
       } else {
-        __stcg(gb + (size_t)cta * PANEL_NB + tid, p);
-        if (cta == 0) __stcg(gb + (size_t)G * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);  // row k
+        __stcg(gb + (size_t)cta * PANEL_NB + tid, pv);
+        if (cta == 0) __stcg(gb + (size_t)G * PANEL_NB + tid, REG ? rowst[tid] : Ps[k * PANEL_LD + tid]);
       }
     }
-    const int CS = CLUSTER ? a.csize : 1;               // CTAs per cluster
-    const int NCL = CLUSTER ? G / CS : 1;               // clusters (> 1: two-level exchange)
-    const int crank = cta % CS, cid = cta / CS;
+    PSTAMP(1);
     if constexpr (CLUSTER) {
       // push: every CTA stores its partial vector (and, single-cluster, CTA 0 row k) into
       // every peer's exchange slot with st.async; each receiver's mbarrier counts the
@@ -195,7 +288,7 @@ panel_qr_kernel_t(const PanelArgs a) {
       __syncthreads();
       if (jj < nb) {
         const double pv = red[PANEL_RG * PANEL_NB + jj];
-        const double rv = cta == 0 ? Ps[k * PANEL_LD + jj] : 0.0;
+        const double rv = cta == 0 ? (REG ? rowst[jj] : Ps[k * PANEL_LD + jj]) : 0.0;
         const uint32_t lpart = smem_u32(xp + 2 * PANEL_NB + crank * PANEL_NB + jj);
         const uint32_t lrow = smem_u32(xp + PANEL_NB + jj);
         const uint32_t lbar = smem_u32(xbar + (k & 1));
@@ -206,65 +299,67 @@ panel_qr_kernel_t(const PanelArgs a) {
         }
       }
     }
+    PSTAMP(2);
     // T column of the previous step (inputs double-buffered), overlapping the exchange
     if (cta == tcta && k > 0)
       panel_t_column(Ts, k - 1, totb + ((k - 1) & 1) * PANEL_NB, drowb + ((k - 1) & 1) * PANEL_NB,
                      sc, tauv);
+    PSTAMP(3);
     if (timed) { t1 = clock64(); ph[0] += t1 - t0; t0 = t1; }
     if constexpr (CLUSTER) {
       xmbar_wait(xbar + (k & 1), (k >> 1) & 1);
-      if (NCL > 1) {
-        // two-level: every CTA forms its cluster's sum (same fixed order); the leaders
-        // publish them (and CTA 0 row k) through L2; one counter arrival per cluster
-        double t = 0.0;
-        if (jj < nb) {
-#pragma unroll
-          for (int u = 0; u < 16 / PANEL_RG; ++u) {
-            const int c = rg + PANEL_RG * u;
-            t += c < CS ? xp[2 * PANEL_NB + c * PANEL_NB + jj] : 0.0;
-          }
-        }
-        red[rg * PANEL_NB + jj] = t;
-        __syncthreads();
-        if (tid < nb && crank == 0) {
-          __stcg(gb + (size_t)cid * PANEL_NB + tid, sum_groups(red, tid));
-          if (cta == 0) __stcg(gb + (size_t)NCL * PANEL_NB + tid, Ps[k * PANEL_LD + tid]);
-        }
-        leaders_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)NCL, crank == 0);
+      PSTAMP(4);
+      if (NCL > 1 && tid < nb && crank == 0) {
+        // two-level: the cluster leaders publish their cluster's sum (and CTA 0 row k)
+        // through L2 as flag-carrying words (read below by every CTA)
+        double* ll = a.ll + (size_t)(k & 1) * 17 * PANEL_NB * 2;
+        const unsigned flag = a.epoch + (unsigned)k + 1u;
+        ll_store(ll + ((size_t)cid * PANEL_NB + tid) * 2, sum_slots(xp + 2 * PANEL_NB + tid, CS), flag);
+        if (cta == 0)
+          ll_store(ll + ((size_t)16 * PANEL_NB + tid) * 2, REG ? rowst[tid] : Ps[k * PANEL_LD + tid], flag);
       }
     } else {
       grid_barrier(a.bar, a.bar_base + (unsigned)(k + 1) * (unsigned)G);
     }
+    PSTAMP(5);
     if (timed) { t1 = clock64(); ph[1] += t1 - t0; t0 = t1; }
-    // row k of the panel (owned by CTA 0): local in cluster mode; in grid mode staged into
-    // shared memory by the rg == last group during the partial-sum loads (same L2 round trip)
-    double* rows = red + PANEL_RG * PANEL_NB;          // staging row (free after the push)
-    const double* row0;
-    if (CLUSTER && NCL == 1) row0 = xp + PANEL_NB;
-    else row0 = rows;
-    if ((!CLUSTER || NCL > 1) && rg == PANEL_RG - 1 && jj < nb)
-      rows[jj] = __ldcg(gb + (size_t)(CLUSTER ? NCL : G) * PANEL_NB + jj);
-    // (b) every CTA sums the per-CTA (per-cluster) partials in the same fixed order
-    if (CLUSTER && NCL > 1) {
-      double t = 0.0;
-      if (jj < nb) {
-#pragma unroll
-        for (int u = 0; u < 16 / PANEL_RG; ++u) {
-          const int c = rg + PANEL_RG * u;
-          t += c < NCL ? __ldcg(gb + (size_t)c * PANEL_NB + jj) : 0.0;
-        }
+    // (b) the column totals tot[j] = sum over all CTAs of part[j] (same fixed order in every
+    // CTA) and row k of the panel (owned by CTA 0) -> totb / drowb (double-buffered by
+    // column parity: the T column of this step reads them during the next exchange)
+    double* totk = totb + (k & 1) * PANEL_NB;
+    double* drowk = drowb + (k & 1) * PANEL_NB;
+    if (CLUSTER && NCL == 1) {
+      if (tid < nb) {
+        totk[tid] = sum_slots(xp + 2 * PANEL_NB + tid, CS);
+        drowk[tid] = xp[PANEL_NB + tid];
       }
-      red[rg * PANEL_NB + jj] = t;
-    } else if constexpr (CLUSTER) {
-      double t = 0.0;
+    } else if (CLUSTER) {
+      // thread (jj, rg) polls the slots of clusters rg and rg + 8 (and rg = 7 row k)
+      double v0 = 0.0, v1 = 0.0;
       if (jj < nb) {
-#pragma unroll
-        for (int u = 0; u < 16 / PANEL_RG; ++u) {
-          const int c = rg + PANEL_RG * u;
-          t += c < G ? xp[2 * PANEL_NB + c * PANEL_NB + jj] : 0.0;
-        }
+        const double* ll = a.ll + (size_t)(k & 1) * 17 * PANEL_NB * 2;
+        const unsigned flag = a.epoch + (unsigned)k + 1u;
+        const bool has0 = rg < NCL, has1 = rg + PANEL_RG < NCL, hasr = rg == PANEL_RG - 1;
+        double rk = 0.0;
+        unsigned polls = 0;
+        bool ok;
+        do {   // all slots in flight per poll: one L2 round trip once they are written
+          ok = true;
+          if (has0) ok &= ll_load(ll + ((size_t)rg * PANEL_NB + jj) * 2, flag, v0);
+          if (has1) ok &= ll_load(ll + ((size_t)(rg + PANEL_RG) * PANEL_NB + jj) * 2, flag, v1);
+          if (hasr) ok &= ll_load(ll + ((size_t)16 * PANEL_NB + jj) * 2, flag, rk);
+          if (!ok && ++polls > (1u << 24)) {   // co-residency violated: flag it, do not hang
+            atomicExch(a.bar + 1, 1u);
+            break;
+          }
+        } while (!ok);
+        if (!has0) v0 = 0.0;
+        if (!has1) v1 = 0.0;
+        if (hasr) drowk[jj] = rk;
       }
-      red[rg * PANEL_NB + jj] = t;
+      red[rg * PANEL_NB + jj] = v0 + v1;
+      __syncthreads();
+      if (tid < nb) totk[tid] = sum_groups(red, tid);
     } else {
       double t = 0.0;
       if (jj < nb) {
@@ -277,26 +372,59 @@ panel_qr_kernel_t(const PanelArgs a) {
           for (int u = 0; u < 8; ++u) t += v[u];
         }
         for (; c < G; c += PANEL_RG) t += __ldcg(gb + (size_t)c * PANEL_NB + jj);
+        if (rg == PANEL_RG - 1) drowk[jj] = __ldcg(gb + (size_t)G * PANEL_NB + jj);
       }
       red[rg * PANEL_NB + jj] = t;
+      __syncthreads();
+      if (tid < nb) totk[tid] = sum_groups(red, tid);
     }
     __syncthreads();
+    PSTAMP(6);
     if (timed) { t1 = clock64(); ph[2] += t1 - t0; t0 = t1; }
     // (c) reflector of column k, computed redundantly by every thread (identical values)
-    const double alpha = row0[k];
-    const double sigma = sum_groups(red, k);
+    const double alpha = drowk[k];
+    const double sigma = totk[k];
     double tau = 0.0, scale = 0.0, beta = alpha;
     if (sigma != 0.0) {
-      const double nrm = sqrt(alpha * alpha + sigma);
+      // beta = -sign(alpha) nrm, tau = (beta - alpha)/beta = 1 + |alpha|/nrm,
+      // scale = 1/(alpha - beta) = sign(alpha)/(|alpha| + nrm): one rsqrt + one reciprocal
+      const double q = fma(alpha, alpha, sigma);
+      const double rn = rsqrt(q);
+      const double nrm = q * rn;
+      const double aa = fabs(alpha);
       beta = alpha < 0.0 ? nrm : -nrm;
-      tau = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
+      tau = fma(aa, rn, 1.0);
+      const double sa = __drcp_rn(aa + nrm);
+      scale = alpha < 0.0 ? -sa : sa;
     }
+    PSTAMP(7);
     if (jj < nb) {
-      const double totj = sum_groups(red, jj);
-      const double drowj = row0[jj];
-      if (rg == 0) { totb[(k & 1) * PANEL_NB + jj] = totj; drowb[(k & 1) * PANEL_NB + jj] = drowj; }
-      if (jj > k) {
+      const double totj = totk[jj];
+      const double drowj = drowk[jj];
+      if (REG && jj > k) {
+        const double w = tau * fma(scale, totj, drowj);
+        const double ws = w * scale;
+#pragma unroll
+        for (int i = 0; i < RPT; i += 2) {             // x_k is 0 at rows <= k
+          const double2 u = *reinterpret_cast<const double2*>(xk + i);
+          p[i] = fma(-ws, u.x, p[i]);
+          p[i + 1] = fma(-ws, u.y, p[i + 1]);
+        }
+        if (cta == 0 && rg == (k & 7)) {               // diagonal row k
+#pragma unroll
+          for (int i = 0; i < 8 && i < RPT; ++i) p[i] -= sel_bit(k >> 3, i) ? w : 0.0;
+        }
+        if (jj == k + 1) {                             // stage x_{k+1} for the next step
+          double* xn = xs + ((k + 1) & 1) * XS + rg * RPT;
+#pragma unroll
+          for (int i = 0; i < RPT; i += 2) *reinterpret_cast<double2*>(xn + i) = make_double2(p[i], p[i + 1]);
+          if (cta == 0) {                              // rows <= k+1 (all inside CTA 0's first 64)
+#pragma unroll
+            for (int i = 0; i < 8 && i < RPT; ++i)
+              if (rg + PANEL_RG * i <= k + 1) xn[i] = 0.0;
+          }
+        }
+      } else if (!REG && jj > k) {
         // H_k applied to column jj: w = tau (P[k][jj] + scale z_jj); rows r > k: P -= w scale x_r
         const double w = tau * fma(scale, totj, drowj);
         const double ws = w * scale;
@@ -317,25 +445,43 @@ panel_qr_kernel_t(const PanelArgs a) {
         if (cta == 0 && rg == 0) Ps[k * PANEL_LD + jj] -= w;      // diagonal row k
       }
     }
+    PSTAMP(8);
+    if constexpr (REG) {
+      if (cta == 0 && rg == (k & 7) && jj == k) {   // beta on the diagonal
+#pragma unroll
+        for (int i = 0; i < 8 && i < RPT; ++i) p[i] = sel_bit(k >> 3, i) ? beta : p[i];
+      }
+      if (cta == 0 && rg == ((k + 1) & 7) && jj < nb && k + 1 < nb) {   // stage row k+1
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8 && i < RPT; ++i) v += sel_bit((k + 1) >> 3, i) ? p[i] : 0.0;
+        rowst[jj] = v;
+      }
+    }
     if (tid == 0) {
       sc[k] = scale;
       tauv[k] = tau;
-      if (cta == 0) { Ps[k * PANEL_LD + k] = beta; a.tau[k] = tau; }
+      if (cta == 0) { if (!REG) Ps[k * PANEL_LD + k] = beta; a.tau[k] = tau; }
     }
     __syncthreads();
+    PSTAMP(9);
     if (timed) { t1 = clock64(); ph[3] += t1 - t0; }
   }
+  const unsigned long long tlend = clock64();
   if (cta == tcta) {
     panel_t_column(Ts, nb - 1, totb + ((nb - 1) & 1) * PANEL_NB, drowb + ((nb - 1) & 1) * PANEL_NB,
                    sc, tauv);
   }
+  if constexpr (REG) {
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int r = rg + PANEL_RG * i;
+      if (r < R && jj < nb) Ps[r * PANEL_LD + jj] = p[i];
+    }
+  }
   if constexpr (CLUSTER) cooperative_groups::this_cluster().sync();  // peers done reading our smem
   else __syncthreads();
-  if (timed) {
-    const int o = cta == 0 ? 0 : 4;
-    for (int q = 0; q < 4; ++q) atomicAdd(a.dbg + o + q, ph[q]);
-    atomicAdd(a.dbg + 8, 1ull);
-  }
+  const unsigned long long tend = clock64();
 
   // write back: R above the diagonal, v = s_j x below it (LAPACK layout), explicit Y, Y^T
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {
@@ -368,11 +514,33 @@ panel_qr_kernel_t(const PanelArgs a) {
       a.Yt[(long long)j + (long long)r * a.ldyt] = 0.0;
     }
   }
+  if (timed) {
+    const int o = cta == 0 ? 0 : 4;
+    for (int q = 0; q < 4; ++q) atomicAdd(a.dbg + o + q, ph[q]);
+#ifdef SDC_PANEL_SUBPHASES
+    if (cta == 0)
+      for (int q = 0; q < 10; ++q) atomicAdd(a.dbg + 20 + q, sp[q]);
+#endif
+    atomicAdd(a.dbg + 8, 1ull);
+    atomicAdd(a.dbg + 9 + (cta == 0 ? 0 : 3), tloop - tstart);       // prologue
+    atomicAdd(a.dbg + 10 + (cta == 0 ? 0 : 3), tlend - tloop - (ph[0] + ph[1] + ph[2] + ph[3]));
+    atomicAdd(a.dbg + 16 + (cta == 0 ? 0 : 1), tend - tlend);        // T tail + cluster sync
+    atomicAdd(a.dbg + 11 + (cta == 0 ? 0 : 3), clock64() - tend);    // write-back
+  }
+}
+
+// rows per thread of the register-resident variant for a given rows_per (0: smem variant)
+inline int panel_rpt(int rows_per) {
+  return rows_per <= 64 ? 8 : rows_per <= 128 ? 16 : rows_per <= 256 ? 32 : 0;
 }
 
 inline size_t panel_smem_bytes(int rows_per) {
+  const int rpt = panel_rpt(rows_per);
   return sizeof(double) * ((size_t)rows_per * PANEL_LD + (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB +
-                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB + 2);
+                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB + 2 +
+                           (rpt ? 2 * PANEL_RG * rpt + PANEL_NB : 0));
 }
 
+#undef PSTAMP
+#undef PSTAMP0
 }  // namespace sdc

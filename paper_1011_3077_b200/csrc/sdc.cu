@@ -73,6 +73,8 @@ struct sdc_handle {
   double *G1 = nullptr, *G2 = nullptr, *G3 = nullptr, *T1 = nullptr, *Ah = nullptr, *Bh = nullptr;
   double *QLb = nullptr, *Rprev = nullptr;
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
+  double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
+  unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
   double *pmA = nullptr, *pmB = nullptr, *vec = nullptr, *scal = nullptr;
   size_t wp_elems = 0;
   unsigned int* bar = nullptr;
@@ -84,6 +86,7 @@ struct sdc_handle {
   int panel_rows = 128;                // target rows per panel CTA
   bool cluster_ok = false;             // 16-CTA clusters usable for the panel kernel
   bool mcluster_ok = false;            // several co-resident 16-CTA clusters (tall panels)
+  bool panel_reg = true;               // register-resident panel column loop (rows_per <= 256)
   int max_clusters16 = 0;
   int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width (multiple of 64)
@@ -463,6 +466,25 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
 // ---------------------------------------------------------------------------------------
 // panel (cooperative) and blocked QR
 // ---------------------------------------------------------------------------------------
+// panel kernel instance: cluster or grid exchange x register (RPT rows/thread) or smem column loop
+const void* panel_fn(bool cluster, int rpt) {
+  if (cluster) {
+    switch (rpt) {
+      case 8: return (const void*)panel_qr_kernel_t<true, 8>;
+      case 16: return (const void*)panel_qr_kernel_t<true, 16>;
+      case 32: return (const void*)panel_qr_kernel_t<true, 32>;
+      default: return (const void*)panel_qr_kernel_t<true, 0>;
+    }
+  }
+  switch (rpt) {
+    case 8: return (const void*)panel_qr_kernel_t<false, 8>;
+    case 16: return (const void*)panel_qr_kernel_t<false, 16>;
+    case 32: return (const void*)panel_qr_kernel_t<false, 32>;
+    default: return (const void*)panel_qr_kernel_t<false, 0>;
+  }
+}
+inline int rpt_slot(int rpt) { return rpt == 8 ? 1 : rpt == 16 ? 2 : rpt == 32 ? 3 : 0; }
+
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
   // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange); taller panels: several
@@ -492,19 +514,21 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
   }
   if (cluster && csize == 1) csize = G;
   size_t smem = panel_smem_bytes(rows_per);
-  static size_t attr_smem[2] = {0, 0};
-  if (smem > attr_smem[cluster]) {
-    cudaError_t e = cudaFuncSetAttribute(cluster ? panel_qr_kernel_t<true> : panel_qr_kernel_t<false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int rpt = h->panel_reg ? panel_rpt(rows_per) : 0;
+  const void* fn = panel_fn(cluster, rpt);
+  static size_t attr_smem[2][4] = {};
+  size_t& cur = attr_smem[cluster][rpt_slot(rpt)];
+  if (smem > cur) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
       set_err("panel: %d rows per CTA need %zu B of shared memory (n too large): %s", rows_per,
               smem, cudaGetErrorString(e));
       return SDC_ERR_NOT_SUPPORTED;
     }
-    attr_smem[cluster] = smem;
+    cur = smem;
   }
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
-              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize};
+              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize, h->llbuf, h->ll_epoch};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   if (cluster) {
     cudaLaunchConfig_t cfg = {};
@@ -519,11 +543,12 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SDC_CK(cudaLaunchKernelEx(&cfg, panel_qr_kernel_t<true>, a));
-    if (G > csize) h->bar_count += (unsigned long long)(G / csize) * nb;
+    void* args[] = {&a};
+    SDC_CK(cudaLaunchKernelExC(&cfg, fn, args));
+    if (G > csize) h->ll_epoch += nb;
   } else {
     void* args[] = {&a};
-    SDC_CK(cudaLaunchCooperativeKernel((const void*)panel_qr_kernel_t<false>, dim3(G),
+    SDC_CK(cudaLaunchCooperativeKernel(fn, dim3(G),
                                        dim3(PANEL_THREADS), args, smem, h->st));
     h->bar_count += (unsigned long long)G * nb;
   }
@@ -803,6 +828,16 @@ int similarity_select(sdc_handle* h, int n, const double* A, long long lda, cons
 }
 
 // synchronise and report a grid-barrier timeout recorded by a panel kernel (bar[1])
+// start of a call: grid-barrier counter and LL exchange flags back to a known state (also
+// inside a captured graph, so every replay starts from the same epochs)
+int reset_sync(sdc_handle* h) {
+  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
+  SDC_CK(cudaMemsetAsync(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
+  h->bar_count = 0;
+  h->ll_epoch = 0;
+  return 0;
+}
+
 int check_barrier(sdc_handle* h) {
   unsigned int err = 0;
   SDC_CK(cudaMemcpyAsync(&err, h->bar + 1, sizeof(err), cudaMemcpyDeviceToHost, h->st));
@@ -834,8 +869,7 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
                  const double* V, long long ldv, const double* VL, long long ldvl) {
   const long long ld = n, m = 2LL * n;
   const bool pencil = B != nullptr;
-  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
-  h->bar_count = 0;
+  SDC_TRY(reset_sync(h));
   SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
   SDC_TRY(norms(h, A, lda, n, h->scal));
   if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
@@ -1015,6 +1049,8 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   ALLOC(h->Wp, h->wp_elems);
   ALLOC(h->W, (size_t)std::max(256, h->nbo) * (n + 64));
   ALLOC(h->gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
+  ALLOC(h->llbuf, PANEL_LL_DOUBLES);
+  if (!rc && cudaMemset(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)) != cudaSuccess) rc = SDC_ERR_CUDA;
   ALLOC(h->pmA, (n / SEL_T + 1) * n);
   if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
   ALLOC(h->vec, 4 * n + 64);
@@ -1033,14 +1069,19 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   }
   if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
   if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
+  if (getenv("SDC_PANEL_SMEM")) h->panel_reg = false;
   if (const char* e = getenv("SDC_GRAPH_MAX_N")) h->graph_max_n = atoi(e);
   if (const char* e = getenv("SDC_CLUSTER_MAX_ROWS")) h->cluster_max_rows = atoi(e);
   if (!rc) {   // non-portable cluster size 16 for the small-panel kernel (if the part allows it)
     int cl = 0;
     cudaDeviceGetAttribute(&cl, cudaDevAttrClusterLaunch, device);
-    if (cl && cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                   1) == cudaSuccess) {
-      cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    bool np = cl != 0;
+    for (int rpt : {0, 8, 16, 32})
+      np = np && cudaFuncSetAttribute(panel_fn(true, rpt), cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                      1) == cudaSuccess;
+    const void* fn16 = panel_fn(true, 0);
+    if (np) {
+      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)panel_smem_bytes(cdiv(h->cluster_max_rows, 16)));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(16);
@@ -1054,14 +1095,13 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, panel_qr_kernel_t<true>, &cfg) == cudaSuccess && ncl >= 1)
+      if (cudaOccupancyMaxActiveClusters(&ncl, fn16, &cfg) == cudaSuccess && ncl >= 1)
         h->cluster_ok = true;
       // tall panels: how many 16-CTA clusters with ~256-row blocks can be resident at once
       cfg.dynamicSmemBytes = panel_smem_bytes(256);
-      cudaFuncSetAttribute(panel_qr_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)panel_smem_bytes(256));
+      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem_bytes(256));
       int ncl2 = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl2, panel_qr_kernel_t<true>, &cfg) == cudaSuccess && ncl2 >= 2) {
+      if (cudaOccupancyMaxActiveClusters(&ncl2, fn16, &cfg) == cudaSuccess && ncl2 >= 2) {
         h->max_clusters16 = ncl2;
         h->mcluster_ok = true;
       }
@@ -1264,8 +1304,7 @@ int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double
   if (lda < m) { set_err("invalid argument (lda < m)"); return -6; }
   if (Qthin && ldq < m) { set_err("invalid argument (Qthin && ldq < m)"); return -8; }
   h->st = static_cast<cudaStream_t>(stream);
-  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
-  h->bar_count = 0;
+  SDC_TRY(reset_sync(h));
   const Fac f{h->Y, (long long)m, h->Yt, (long long)n};
   SDC_TRY(blocked_qr(h, A, lda, m, n, f));
   if (Qthin) {
@@ -1290,8 +1329,7 @@ int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, c
   if (Rout && ldr < n) { set_err("invalid argument (Rout && ldr < n)"); return -13; }
   h->st = static_cast<cudaStream_t>(stream);
   const long long m = 2LL * n;
-  SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
-  h->bar_count = 0;
+  SDC_TRY(reset_sync(h));
   k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, A, lda, B, ldb, n);
   SDC_LAUNCHED(h);
   SDC_TRY(irs_pass(h, n, A, lda, B, ldb, Aout, ldao, Bout, ldbo, h->S, -1, Rout, ldr));
