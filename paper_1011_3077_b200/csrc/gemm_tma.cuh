@@ -34,15 +34,23 @@ struct TmaGemmArgs {
   double* D2; long long ldd2; double alpha2;
   int kchunk;             // K per z-slice (multiple of 16)
   long long c_zstride;    // element stride between z-slices of C
+  int red_ok;             // RED tiles: C += alpha A^T B may use bulk reduce-add (host-checked)
 };
 
 // CPRE: the C tile (beta != 0) is brought into shared memory by TMA at kernel start, in
 // 16-row boxes with the same 128B swizzle, so the epilogue of short-K updates (K <= 256,
 // C -= Y W) reads C on-chip instead of exposing HBM/L2 latency after the main loop.
-template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1, bool CPRE_ = false>
+// RED (persistent kernel): when beta == 1 the epilogue never reads C: each warp stages
+// alpha*acc column segments in shared memory and the bulk-copy engine adds them into C in
+// L2 (cp.reduce.async.bulk .add.f64, round-to-nearest: the same RN(C + alpha*acc) as the
+// load/FMA/store epilogue, bit for bit), so no C load latency is exposed after the K loop.
+template <int BM_, int BN_, int WM_, int WN_, int STAGES_, int MINB_ = 1, bool CPRE_ = false,
+          bool RED_ = false>
 struct TmaTile {
   static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
-  static constexpr bool CPRE = CPRE_;
+  static constexpr bool CPRE = CPRE_, RED = RED_;
+  static constexpr int RED_LD = WM + 2;               // staged column stride (conflict-free)
+  static constexpr int RED_WARP = RED ? 2 * 8 * RED_LD : 0;   // 2 buffers x 8 columns
   static constexpr int BK = 16;                       // one 128-byte swizzle row of doubles
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int CWARPS = WARPS_M * WARPS_N;    // all warps consume
@@ -51,7 +59,8 @@ struct TmaTile {
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int C_BYTES = CPRE ? BM * BN * 8 : 0;
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + C_BYTES + 2 * STAGES * 8 + 16 + 1024;
+  static constexpr size_t SMEM =
+      (size_t)STAGES * STAGE_BYTES + C_BYTES + (size_t)CWARPS * RED_WARP * 8 + 2 * STAGES * 8 + 16 + 1024;
 };
 
 SDC_DEV void mbar_init(uint64_t* bar, unsigned count) {
@@ -89,8 +98,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const TmaGemmArgs g) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms); offset arithmetic on the __shared__ pointer keeps
+  // the address space visible to the compiler, so fragment loads are LDS, not generic LD
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* sC = reinterpret_cast<double*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES + T::C_BYTES);
   uint64_t* empty = full + T::STAGES;
@@ -251,12 +261,17 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
                            const __grid_constant__ CUtensorMap tmB, const TmaGemmArgs g) {
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  // 1024-byte aligned (128B-swizzle atoms); offset arithmetic on the __shared__ pointer keeps
+  // the address space visible to the compiler, so fragment loads are LDS, not generic LD
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* sred = reinterpret_cast<double*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES +
+                                               (size_t)T::CWARPS * T::RED_WARP * 8);
   uint64_t* empty = full + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tx = (g.M + T::BM - 1) / T::BM, ty = (g.N + T::BN - 1) / T::BN;
+  const bool red = T::RED && g.red_ok && g.beta == 1.0 && g.D2 == nullptr;
+  unsigned red_chunk = 0;                      // this warp's staged chunks so far (buffer parity)
   const int tz = (g.K + g.kchunk - 1) / g.kchunk;
   const int ntiles = tx * ty * tz;
 
@@ -331,7 +346,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
     decode(t, m0, n0, z);
     const int nk = ktiles_of(z);
     double* __restrict__ C = g.C + (long long)z * g.c_zstride;
-    if (g.beta != 0.0) {   // warm L2 with this tile's C while its K loop runs
+    if (g.beta != 0.0 && !red) {   // warm L2 with this tile's C while its K loop runs
       constexpr int LPC = (T::BM * 8 + 127) / 128;
       for (int e = threadIdx.x; e < LPC * T::BN; e += T::THREADS) {
         const int n = n0 + e / LPC, m = m0 + (e % LPC) * 16;
@@ -368,6 +383,35 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
       if (lane == 0) mbar_arrive(empty + s);
     }
     // epilogue
+    if constexpr (T::RED) {
+      if (red) {
+        const int mw = m0 + wm * T::WM;                        // this warp's first row
+        const int rows = min(T::WM, g.M - mw);                 // even (host: M even)
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j, ++red_chunk) {
+          double* buf = sred + (size_t)warp * T::RED_WARP + (red_chunk & 1) * 8 * T::RED_LD;
+          // the bulk reads of the chunk staged two steps ago (same buffer) must be done
+          if (lane < 8) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              buf[(h ? c1 : c0) * T::RED_LD + i * 8 + fr] = g.alpha * acc[i][j][h];
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          const int n = n0 + wn * T::WN + j * 8 + lane;
+          if (lane < 8 && rows > 0 && n < g.N) {
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(
+                             C + mw + (long long)n * g.ldc),
+                         "r"(smem_u32(buf + lane * T::RED_LD)), "r"(rows * 8)
+                         : "memory");
+          }
+          if (lane < 8) asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        continue;
+      }
+    }
     const bool use_beta = g.beta != 0.0;
 #pragma unroll
     for (int i = 0; i < T::MI; ++i) {
@@ -397,6 +441,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
         }
     }
   }
+  if (T::RED && red && lane < 8) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 }  // namespace sdc

@@ -216,6 +216,7 @@ using TmaM = TmaTile<64, 128, 32, 32, 6>;       // M <= 64 (W0 = Y^T C), 8 consu
 using TmaS = TmaTile<64, 64, 32, 32, 6>;        // small grids, 4 consumer warps
 using TmaU = TmaTile<128, 64, 64, 32, 4, 2>;    // rank-nb updates: 2 CTAs/SM, epilogue overlap
 using TmaC = TmaTile<128, 128, 64, 32, 3, 1, true>;  // K <= 256 updates, C tile prefetched by TMA
+using TmaR = TmaTile<128, 64, 64, 32, 3, 2, false, true>;  // updates with beta = 1: bulk reduce-add
 
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
@@ -337,6 +338,15 @@ int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const doub
   return 0;
 }
 
+int red_mode() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SDC_RED");
+    v = e ? atoi(e) : 1;   // bulk reduce-add epilogue for beta = 1 updates
+  }
+  return v;
+}
+
 int persist_mode() {
   static int v = -2;
   if (v == -2) {
@@ -356,7 +366,8 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (splits <= 1) { splits = 1; kchunk = std::max(K, 1); }
   const bool tma = K > 0 && al16(A, lda) && al16(B, ldb) && tma_encode_fn() != nullptr;
   if (tma) {
-    TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride};
+    TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
+                  (int)(al16(C, ldc) && M % 2 == 0)};
     int v = gemm_variant_override();
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
@@ -373,7 +384,10 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
         case 0: return launch_tma_persist<TmaL>(h, A, lda, B, ldb, g, splits);
         case 1: return launch_tma_persist<TmaM>(h, A, lda, B, ldb, g, splits);
         case 2: return launch_tma_persist<TmaS>(h, A, lda, B, ldb, g, splits);
-        case 3: return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
+        case 3:
+          if (red_mode() && beta == 1.0 && D2 == nullptr && g.red_ok)
+            return launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
+          return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
         default: break;
       }
     }

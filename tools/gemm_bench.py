@@ -17,20 +17,24 @@ def main():
               ("TN rank-64 update", True, False, 2 * n, n, 64),
               ("TN rank-128 update", True, False, 2 * n, n, 128),
               ("TN rank-256 update", True, False, 2 * n, n, 256),
+              ("TN rank-256 update b=0", True, False, 2 * n, n, -256),
               ("TN W0 (no split-K)", True, False, 64, n, 2 * n)]
     for name, ta, tb, M, N, K in shapes:
+        beta = 1.0
+        if K < 0:
+            K, beta = -K, 0.0
         A = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, device=dev, generator=g)
         B = torch.randn((N, K) if tb else (K, N), dtype=torch.float64, device=dev, generator=g)
         A, B = api.colmajor(A), api.colmajor(B)
         C = api.empty_colmajor(M, N, dev)
         C.zero_()
         for _ in range(2):
-            h.dgemm(A, B, ta, tb, alpha=-1.0, beta=1.0, C=C)
+            h.dgemm(A, B, ta, tb, alpha=-1.0, beta=beta, C=C)
         torch.cuda.synchronize()
         h.profile(True)
         reps = 5
         for _ in range(reps):
-            h.dgemm(A, B, ta, tb, alpha=-1.0, beta=1.0, C=C)
+            h.dgemm(A, B, ta, tb, alpha=-1.0, beta=beta, C=C)
         ms, cnt, fl = h.profile_read(0)
         h.profile(False)
         print(f"{name:24s} M={M} N={N} K={K}: {ms / cnt:8.3f} ms  {fl / (ms / 1e3) / 1e12:6.2f} TFLOP/s")
