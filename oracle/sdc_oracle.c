@@ -33,6 +33,10 @@
 #include <string.h>
 
 #define EL(a, i, j, ld) ((a)[(size_t)(j) * (size_t)(ld) + (size_t)(i)])
+/* OpenMP only for large problems (thread start-up dominates tiny ones).  Scheduling only:
+ * every output element is still computed by one thread in the same loop order, so the
+ * results do not depend on this threshold or on the thread count. */
+#define ORC_PAR_MIN 65536L
 
 static double sgn_nonneg(double x) { return x < 0.0 ? -1.0 : 1.0; } /* sign(0)=+1 (Q7) */
 
@@ -66,7 +70,7 @@ void orc_geqr2(int m, int n, double *A, int lda, double *tau) {
     larfg(m - k - 1, &EL(A, k, k, lda), &EL(A, k + 1, k, lda), 1, &tau[k]);
     double t = tau[k];
     if (t == 0.0) continue;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)m * n >= ORC_PAR_MIN)
     for (int j = k + 1; j < n; ++j) {           /* apply H_k to column j */
       double w = EL(A, k, j, lda);
       for (int i = k + 1; i < m; ++i) w += EL(A, i, k, lda) * EL(A, i, j, lda);
@@ -82,7 +86,7 @@ void orc_geqr2(int m, int n, double *A, int lda, double *tau) {
 static void apply_qr_reflector(int m, int k, const double *Y, int ldy, double tau,
                                double *C, int ldc, int c0, int c1) {
   if (tau == 0.0) return;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)m * (c1 - c0) >= ORC_PAR_MIN)
   for (int j = c0; j < c1; ++j) {
     double w = EL(C, k, j, ldc);
     for (int i = k + 1; i < m; ++i) w += EL(Y, i, k, ldy) * EL(C, i, j, ldc);
@@ -135,7 +139,7 @@ void orc_gerq2(int n, double *A, int lda, double *tau) {
     double t = tau[i];
     if (t == 0.0) continue;
     /* A(0:i-1, 0:i) <- A(0:i-1, 0:i) (I - t v v^T), v = [A(i,0:i-1), 1] */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
     for (int r = 0; r < i; ++r) {
       double w = EL(A, r, i, lda);
       for (int c = 0; c < i; ++c) w += EL(A, r, c, lda) * EL(A, i, c, lda);
@@ -155,7 +159,7 @@ void orc_orgr2_signed(int n, const double *Y, int ldy, const double *tau, double
   for (int i = n - 1; i >= 0; --i) {
     double t = tau[i];
     if (t == 0.0) continue;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
     for (int j = 0; j < n; ++j) {
       double w = EL(Q, i, j, ldq);
       for (int c = 0; c < i; ++c) w += EL(Y, i, c, ldy) * EL(Q, c, j, ldq);
@@ -181,7 +185,7 @@ void orc_geql2(int n, double *A, int lda, double *tau) {
     double t = tau[i];
     if (t == 0.0) continue;
     /* A(0:i, 0:i-1) <- (I - t v v^T) A(0:i, 0:i-1), v = [A(0:i-1,i); 1] */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
     for (int j = 0; j < i; ++j) {
       double w = EL(A, i, j, lda);
       for (int r = 0; r < i; ++r) w += EL(A, r, i, lda) * EL(A, r, j, lda);
@@ -201,7 +205,7 @@ void orc_org2l_signed(int n, const double *Y, int ldy, const double *tau, double
   for (int i = 0; i < n; ++i) {
     double t = tau[i];
     if (t == 0.0) continue;
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
     for (int j = 0; j < n; ++j) {
       double w = EL(Q, i, j, ldq);
       for (int r = 0; r < i; ++r) w += EL(Y, r, i, ldy) * EL(Q, r, j, ldq);
@@ -222,7 +226,7 @@ void orc_org2l_signed(int n, const double *Y, int ldy, const double *tau, double
  * ---------------------------------------------------------------------------------- */
 void orc_gemm(int ta, int tb, int m, int n, int K, const double *A, int lda,
               const double *B, int ldb, double *C, int ldc) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if ((long)m * n * K / 64 >= ORC_PAR_MIN)
   for (int j = 0; j < n; ++j) {
     for (int i = 0; i < m; ++i) {
       double s = 0.0;
