@@ -206,7 +206,7 @@ def main():
     cfg_name = f"cfg{cfg}: " + inputs.CONFIG_DOC[cfg] + ("" if args.n is None else f" [n overridden to {n}]")
 
     if args.impl == "reference":
-        passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30}[cfg]
+        passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30, 6: 30}[cfg]
         return run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg)
 
     import numpy as np
@@ -220,7 +220,13 @@ def main():
     dev = torch.device("cuda", local)
 
     t_in = time.perf_counter()
-    p = inputs.make_config(cfg, n=n, device=dev)
+    svd = cfg == 6
+    if svd:   # singular-value split: the RSEP step on the order-n embedding of an (n/2)^2 A
+        A6, V6, _, s6, _ = inputs.svd_known(n // 2, n // 2, 8, 1008, device=dev)
+        p = inputs.Problem("cfg6", n, A6, None, V6, None, 30, 0.0, 0,
+                           expected_k=2 * int(np.sum(s6 < 1)))
+    else:
+        p = inputs.make_config(cfg, n=n, device=dev)
     passes = args.passes or p.max_iters
     stop = {0: "fixed", 1: "rtest", 2: "e21"}[p.stop]
     torch.cuda.synchronize()
@@ -230,6 +236,9 @@ def main():
     QL = api.empty_colmajor(n, n, dev) if pencil else None
 
     def step():
+        if svd:
+            q, _, info = h.svd_split(p.A, 1.0, p.V, max_iters=passes, Q=Q)
+            return q, None, None, info
         return h.split(p.A, p.B, p.V, p.VL, max_iters=passes, tol=p.tol, stop=stop, Q=Q, QL=QL)
 
     def barrier():
@@ -275,7 +284,30 @@ def main():
 
     # ---- end to end: host buffers through the C ABI, copies inside the timed region ----
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and svd:
+        # public Python API: pinned host A -> device, svd_split, Q -> pinned host, per step
+        m6 = n // 2
+        hA = torch.empty((m6, m6), dtype=torch.float64, pin_memory=True)
+        hA.copy_(p.A.t())
+        hQ = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        dA = torch.empty((m6, m6), dtype=torch.float64, device=dev)
+
+        def e2e_step():
+            dA.copy_(hA, non_blocking=True)
+            q, _, _ = h.svd_split(dA.t(), 1.0, p.V, max_iters=passes, Q=Q)
+            hQ.copy_(q.t(), non_blocking=True)
+        e2e_step()
+        barrier()
+        e0.record(st)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(st)
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
+        e2e = {"value": replica_throughput(ms_e2e, world), "unit": "split steps/s",
+               "h2d_bytes_per_step": m6 * m6 * 8, "d2h_bytes_per_step": n * n * 8,
+               "ms_per_step": ms_e2e, "steps": args.e2e_steps}
+    elif args.e2e_steps > 0:
         def pinned(x):
             if x is None:
                 return None

@@ -119,6 +119,28 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
                      double* Q, int ldq, double* QL, int ldql, double* Ahat, int ldah, double* hist,
                      int hist_cap, sdc_result* res);
 
+/* Singular-value split ("construct the hermitian matrix [[0, A], [A^H, 0]]
+ * and compute its eigenvalues (which are the singular values of A and their negatives)";
+ * SURVEY §8(f) row f3): the m x n matrix A is embedded on the device into the order
+ * N = m + n symmetric H = [[0, A], [A^T, 0]] and one RSEP step (Alg. 6, PAPER.md:436-447:
+ * the unit-disk step with Ahat := (Ahat + Ahat^T)/2) splits H along |z| = rho.
+ *  1 h          handle with n_max >= m + n
+ *  2 stream
+ *  3 m, 4 n     rows / columns of A (>= 1)
+ *  5 A, 6 lda   input (device), lda >= m
+ *  7 rho        > 0, finite: the threshold on the singular values
+ *  8 V, 9 ldv   Haar V of order N for GRURV (ldv >= N)
+ * 10 max_iters, 11 tol, 12 stop_mode   as sdc_split
+ * 13 Q, 14 ldq  out (device): N x N orthogonal; Q(:, r:N-1) spans {[u_i; +-v_i] : sigma_i < rho}
+ *               plus the null vectors of H: its rows 0..m-1 span the left and its rows m..N-1
+ *               the right singular vectors of the singular values below rho
+ * 15 Ahat,16 ldah optional out (device): the symmetrised Q^T H Q (N x N)
+ * 17 hist, 18 hist_cap, 19 res   as sdc_split; res->k = 2 #{sigma_i < rho} + |m - n|
+ * Workspace: an N x N embedding buffer (n_max^2 doubles) is allocated on first use. */
+int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, int lda, double rho,
+                  const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
+                  int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
+
 /* Same step with HOST matrices (column-major, tightly packed ld = n): copies A, B, V, VL to
  * the device, runs sdc_split, and copies Q (and QL, Ahat when non-NULL) back -- the
  * end-to-end path of the public API.  Host buffers may be pageable or pinned. */

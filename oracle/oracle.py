@@ -56,6 +56,9 @@ def lib():
             _lib.orc_split_region.restype = I
             _lib.orc_split_region.argtypes = [I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I,
                                               P, I, P, I, ctypes.POINTER(_Result)]
+            _lib.orc_svd_split.restype = I
+            _lib.orc_svd_split.argtypes = [I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,
+                                           ctypes.POINTER(_Result)]
             _lib.orc_split_select.restype = D
             _lib.orc_split_select.argtypes = [I, P, I, D, P, I, D, ctypes.POINTER(I), P]
             _lib.orc_norm1.restype = D
@@ -252,4 +255,24 @@ def split(A, B=None, V=None, VL=None, max_iters=12, tol=0.0, stop=STOP_FIXED,
     if rc != 0:
         raise ValueError(f"orc_split returned {rc}")
     return SplitResult(Q, QL, Ah, res.k, res.r, res.metric, res.metric_fro, res.iters,
+                       res.converged, res.status, hist)
+
+
+def svd_split(A, rho, V, max_iters=12, tol=0.0, stop=STOP_FIXED, hist_cap=None) -> SplitResult:
+    """Singular values of the m x n A below rho: RSEP step on [[0, A], [A^T, 0]]
+    (PAPER.md:453); mirrors sdc_svd_split.  Q and Ahat are (m+n) x (m+n)."""
+    A = _f(A)
+    m, n = A.shape
+    N = m + n
+    V = _f(V)
+    hist_cap = max_iters if hist_cap is None else hist_cap
+    Q = np.zeros((N, N), order="F")
+    Ah = np.zeros((N, N), order="F")
+    hist = np.full((hist_cap, 3), np.nan)
+    res = _Result()
+    rc = lib().orc_svd_split(m, n, _p(A), m, float(rho), _p(V), N, max_iters, float(tol), int(stop),
+                             _p(Q), N, _p(Ah), N, _p(hist), hist_cap, ctypes.byref(res))
+    if rc != 0:
+        raise ValueError(f"orc_svd_split returned {rc}")
+    return SplitResult(Q, None, Ah, res.k, res.r, res.metric, res.metric_fro, res.iters,
                        res.converged, res.status, hist)

@@ -567,3 +567,29 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   if (pencil) { free(Lj); free(Mj); free(Bh); free(QLw); }
   return 0;
 }
+
+/* Singular-value split: "construct the hermitian matrix
+ * B = [[0, A], [A^H, 0]] and compute its eigenvalues (which are the singular values of A
+ * and their negatives)".  The m x n matrix A is embedded into the (m+n) x (m+n) symmetric
+ * H = [[0, A], [A^T, 0]] and one RSEP step (Alg. 6: IRS(H, I), GRURV,
+ * Ahat = Q^T H Q, Ahat := (Ahat + Ahat^T)/2, split selection) splits it along |z| = rho.
+ * k = #{|eig(H)| < rho} = 2 #{sigma_i < rho} + |m - n|. */
+int orc_svd_split(int m, int n, const double *A, int lda, double rho,
+                  const double *V, int ldv, int max_iters, double tol, int stop_mode,
+                  double *Q, int ldq, double *Ahat_out, int ldah,
+                  double *hist, int hist_cap, orc_result *res) {
+  if (m < 1 || n < 1) return -1;
+  if (lda < m) return -4;
+  const int N = m + n;
+  double *H = (double *)calloc((size_t)N * N, sizeof(double));
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < m; ++i) {
+      EL(H, i, m + j, N) = EL(A, i, j, lda);      /* H(0:m, m:m+n) = A   */
+      EL(H, m + j, i, N) = EL(A, i, j, lda);      /* H(m:m+n, 0:m) = A^T */
+    }
+  int rc = orc_split_region(N, H, N, NULL, 0, V, ldv, NULL, 0, ORC_REGION_DISK, rho,
+                            ORC_FLAG_SYMMETRIC, max_iters, tol, stop_mode, Q, ldq, NULL, 0,
+                            Ahat_out, ldah, hist, hist_cap, res);
+  free(H);
+  return rc;
+}

@@ -59,6 +59,12 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
                      double *Q, int ldq, double *QLout, int ldql, double *Ahat_out, int ldah,
                      double *hist, int hist_cap, orc_result *res);
 
+/* singular values below rho: RSEP step on [[0, A], [A^T, 0]] */
+int orc_svd_split(int m, int n, const double *A, int lda, double rho,
+                  const double *V, int ldv, int max_iters, double tol, int stop_mode,
+                  double *Q, int ldq, double *Ahat_out, int ldah,
+                  double *hist, int hist_cap, orc_result *res);
+
 #ifdef __cplusplus
 }
 #endif

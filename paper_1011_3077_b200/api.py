@@ -133,6 +133,30 @@ class Handle:
                          res.status, hist)
         return Q, QL, Ah, info
 
+    def svd_split(self, A, rho, V, max_iters=12, tol=0.0, stop="fixed", Q=None, want_ahat=False,
+                  hist_cap=None):
+        """sdc_svd_split: singular values of the m x n A below rho.
+        Returns (Q (m+n)x(m+n), Ahat or None, SplitInfo); info.k = 2 #{sigma < rho} + |m-n|."""
+        m, n = A.shape
+        N = m + n
+        dev = A.device
+        A, V = colmajor(A), colmajor(V)
+        Q = empty_colmajor(N, N, dev) if Q is None else Q
+        Ah = empty_colmajor(N, N, dev) if want_ahat else None
+        hist_cap = max_iters if hist_cap is None else hist_cap
+        hist = np.full((hist_cap, 3), np.nan)
+        res = SdcResult()
+        pa, la = _ptr_ld(A)
+        pv, lv = _ptr_ld(V)
+        pq, lq = _ptr_ld(Q)
+        pah, lah = _ptr_ld(Ah)
+        rc = self.lib.sdc_svd_split(self._h, _stream(dev), m, n, pa, la, float(rho), pv, lv,
+                                    max_iters, float(tol), STOPS[stop], pq, lq, pah, lah,
+                                    hist.ctypes.data_as(ctypes.c_void_p), hist_cap, ctypes.byref(res))
+        check(rc, "sdc_svd_split")
+        return Q, Ah, SplitInfo(res.k, res.r, res.metric, res.metric_fro, res.iters, res.converged,
+                                res.status, hist)
+
     def split_host(self, A: np.ndarray, B=None, V=None, VL=None, max_iters=12, tol=0.0,
                    stop="fixed", Q=None, QL=None, want_ahat=False, stream=None):
         """sdc_split_host on host (numpy, Fortran-ordered fp64) buffers: the end-to-end path."""

@@ -39,6 +39,19 @@ __global__ void k_copy(double* out, long long ldo, const double* src, long long 
   }
 }
 
+// hermitian embedding for the singular-value split:
+//   H = [[0, A], [A^T, 0]]  (N = m + n, ld N), A m x n
+__global__ void k_embed(double* H, const double* A, long long lda, int m, int n) {
+  const int N = m + n;
+  SDC_FOR_MN(N, N) {
+    const int i = (int)(_e % N), j = (int)(_e / N);
+    double v = 0.0;
+    if (i < m && j >= m) v = A[i + (long long)(j - m) * lda];
+    else if (i >= m && j < m) v = A[j + (long long)(i - m) * lda];
+    H[i + (long long)j * N] = v;
+  }
+}
+
 // tiled transpose-with-remap:  out(i, j) = s(j) * src(ri(i, j), rj(i, j)) where the mode
 // selects the remap (used for RQ = reversed QR of C^T J and QL = reversed QR of J X J):
 //   mode 0: out(i,j) = src(j, i)                      (transpose)

@@ -72,6 +72,7 @@ struct sdc_handle {
   double *AL[2] = {nullptr, nullptr}, *BL[2] = {nullptr, nullptr};
   double *G1 = nullptr, *G2 = nullptr, *G3 = nullptr, *T1 = nullptr, *Ah = nullptr, *Bh = nullptr;
   double *QLb = nullptr, *Rprev = nullptr;
+  double* Emb = nullptr;               // hermitian embedding of sdc_svd_split (lazy, n_max^2)
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
   double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
   unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
@@ -1139,6 +1140,38 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
   if (region != SDC_REGION_UNIT_DISK) { set_err("sdc_split: use sdc_split_region for region %d", region); return -12; }
   return sdc_split_region(h, stream, n, A, lda, B, ldb, V, ldv, VL, ldvl, region, 1.0, 0, max_iters,
                           tol, stop_mode, Q, ldq, QL, ldql, Ahat, ldah, hist, hist_cap, res);
+}
+
+int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, int lda, double rho,
+                  const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
+                  int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res) {
+  SDC_TRY(check_handle(h));
+  if (m < 1) { set_err("m < 1"); return -3; }
+  if (n < 1) { set_err("n < 1"); return -4; }
+  if (m + n > h->n_max) { set_err("m + n = %d exceeds n_max = %d", m + n, h->n_max); return -4; }
+  if (!A) { set_err("A is NULL"); return -5; }
+  if (lda < m) { set_err("lda < m"); return -6; }
+  if (!(rho > 0.0) || !std::isfinite(rho)) { set_err("rho must be finite and > 0"); return -7; }
+  const int N = m + n;
+  if (!h->Emb) SDC_TRY(dalloc(h, &h->Emb, (size_t)h->n_max * h->n_max));
+  h->st = static_cast<cudaStream_t>(stream);
+  k_embed<<<ew_grid((long long)N * N), 256, 0, h->st>>>(h->Emb, A, lda, m, n);
+  SDC_LAUNCHED(h);
+  const int rc = sdc_split_region(h, stream, N, h->Emb, N, nullptr, 0, V, ldv, nullptr, 0,
+                                  SDC_REGION_DISK, rho, SDC_FLAG_SYMMETRIC, max_iters, tol, stop_mode,
+                                  Q, ldq, nullptr, 0, Ahat, ldah, hist, hist_cap, res);
+  // argument positions of the inner call map back onto this signature
+  if (rc == -8) return -8;
+  if (rc == -9) return -9;
+  if (rc == -13) return -10;
+  if (rc == -14) return -11;
+  if (rc == -15) return -12;
+  if (rc == -16) return -13;
+  if (rc == -17) return -14;
+  if (rc == -21) return -16;
+  if (rc == -23) return -18;
+  if (rc == -24) return -19;
+  return rc;
 }
 
 int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,

@@ -147,8 +147,10 @@ CONFIG_DOC = {
     3: "n=4096 Ginibre N(0,2/n) seed 3, V seed 1003, stop when ||E21||_1/||A||_1 <= 1e-13 or 30 passes",
     4: "n=8192 pencil A,B ~ N(0,1) seeds 4,5, V_R seed 1004, V_L seed 2004, 30 passes",
     5: "n=16384 A = U T U^T (seed 6), |lam| in [.2,.8] (n/2) and [1.25,5] (n/2), V seed 1006, 30 passes, k=8192",
+    6: "singular-value split (f3, PAPER.md:453): A 8192x8192 = U diag(s) W^T (seed 8), s in [.05,.8] (half) "
+       "and [1.25,20], rho=1, RSEP step on the order-16384 embedding [[0,A],[A^T,0]], V seed 1008, 30 passes",
 }
-CONFIG_N = {1: 64, 2: 1024, 3: 4096, 4: 8192, 5: 16384}
+CONFIG_N = {1: 64, 2: 1024, 3: 4096, 4: 8192, 5: 16384, 6: 16384}
 
 
 def make_config(cfg: int, n: int | None = None, device=None) -> Problem:
@@ -252,3 +254,32 @@ EXPERIMENTS = {
     "E3": dict(fn=imag_axis_eigs, n=25, seed=103, vseed=1103, passes=60),
     "E4": dict(fn=jordan_case, n=32, seed=104, vseed=1104, passes=60),
 }
+
+
+# ---------------------------------------------------------------------------------------
+# singular-value split: A = U[:, :p] diag(s) W^T with
+# Haar U (m x m), W (n x n), p = min(m, n); s log-uniform, half in [.05, .8], half in
+# [1.25, 20] (bounded away from rho = 1, like configs[4]'s eigenvalue annuli).
+# ---------------------------------------------------------------------------------------
+def svd_known(m: int, n: int, seed: int, vseed: int, device=None):
+    """-> (A m x n, V (m+n) x (m+n) Haar for the split, U, s, W) with A = U[:, :p] diag(s) W^T."""
+    rng = np.random.default_rng(seed)
+    p = min(m, n)
+    lo = np.exp(rng.uniform(np.log(0.05), np.log(0.8), p // 2))
+    hi = np.exp(rng.uniform(np.log(1.25), np.log(20.0), p - p // 2))
+    s = rng.permutation(np.concatenate([lo, hi]))
+    if device is None or str(device) == "cpu":
+        U = haar(rng.standard_normal((m, m)))
+        W = haar(rng.standard_normal((n, n)))
+        A = (U[:, :p] * s[None, :]) @ W[:, :p].T
+        V = haar(np.random.default_rng(vseed).standard_normal((m + n, m + n)))
+        return _finish(A, None), _finish(V, None), U, s, W
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    U = haar(torch.randn((m, m), dtype=torch.float64, device=device, generator=g), device)
+    W = haar(torch.randn((n, n), dtype=torch.float64, device=device, generator=g), device)
+    st = torch.as_tensor(s, dtype=torch.float64, device=device)
+    A = (U[:, :p] * st[None, :]) @ W[:, :p].T
+    gv = torch.Generator(device=device).manual_seed(vseed)
+    V = haar(torch.randn((m + n, m + n), dtype=torch.float64, device=device, generator=gv), device)
+    return _finish(A, device), _finish(V, device), U, s, W
