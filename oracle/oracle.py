@@ -76,6 +76,7 @@ def lib():
                 "orc_irs_pass": [I, P, I, P, I, P, I, P, I, P],
                 "orc_grurv_right": [I, P, I, P, I, P, I, P, I, P, P],
                 "orc_grurv_left": [I, P, I, P, I, P, I, P, I],
+                "orc_trevc": [I, P, I, P, I, P, I],
             }.items():
                 f = getattr(_lib, name)
                 f.restype = None
@@ -276,3 +277,14 @@ def svd_split(A, rho, V, max_iters=12, tol=0.0, stop=STOP_FIXED, hist_cap=None) 
         raise ValueError(f"orc_svd_split returned {rc}")
     return SplitResult(Q, None, Ah, res.k, res.r, res.metric, res.metric_fro, res.iters,
                        res.converged, res.status, hist)
+
+
+def trevc(T, Q=None):
+    """Eigenvectors X (upper triangular, X_jj = 1) of the upper triangular T, TX = XD
+    (PAPER.md:1018-1027); Q X when Q is given (eigenvectors of A = Q T Q^T)."""
+    T = _f(T)
+    n = T.shape[0]
+    Qf = None if Q is None else _f(Q)
+    X = np.zeros((n, n), order="F")
+    lib().orc_trevc(n, _p(T), n, _p(Qf), n, _p(X), n)
+    return X

@@ -593,3 +593,37 @@ int orc_svd_split(int m, int n, const double *A, int lda, double rho,
   free(H);
   return rc;
 }
+
+/* TREVC (eq. (trevc)): eigenvectors of an upper triangular T,
+ * TX = XD with D = diag(T), X upper triangular with X_jj = 1 ("X_jj can be
+ * arbitrarily chosen"), for i < j:
+ *   X_ij = (T_ij X_jj + sum_{k=i+1}^{j-1} T_ik X_kj) / (T_jj - T_ii)
+ * evaluated exactly in that order.  Near-equal eigenvalues (reading Q19, the
+ * LAPACK dtrevc/dlaln2 rule): if |T_ii - T_jj| < smin = max(ulp |T_jj|, smlnum) the
+ * denominator T_ii - T_jj is replaced by smin, i.e. X_ij = -(numerator) / smin, with
+ * ulp = 2^-52 and smlnum = DBL_MIN n / ulp.  If Q != NULL the eigenvectors of
+ * A = Q T Q^T are returned instead: X := Q X. */
+void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double *X, int ldx) {
+  const double ulp = 2.220446049250313e-16, smlnum = 2.2250738585072014e-308 * (double)n / ulp;
+  double *Xt = (double *)calloc((size_t)n * n, sizeof(double));
+#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
+  for (int j = 0; j < n; ++j) {
+    const double d = EL(T, j, j, ldt);
+    const double smin = fmax(ulp * fabs(d), smlnum);
+    EL(Xt, j, j, n) = 1.0;
+    for (int i = j - 1; i >= 0; --i) {
+      double num = EL(T, i, j, ldt) * EL(Xt, j, j, n);
+      for (int k = i + 1; k <= j - 1; ++k) num += EL(T, i, k, ldt) * EL(Xt, k, j, n);
+      double den = EL(T, i, i, ldt) - d;               /* (T_ii - T_jj) x = -num */
+      if (fabs(den) < smin) den = smin;
+      EL(Xt, i, j, n) = -num / den;
+    }
+  }
+  if (Q) {
+    orc_gemm(0, 0, n, n, n, Q, ldq, Xt, n, X, ldx);
+  } else {
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) EL(X, i, j, ldx) = EL(Xt, i, j, n);
+  }
+  free(Xt);
+}

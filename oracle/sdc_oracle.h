@@ -65,6 +65,9 @@ int orc_svd_split(int m, int n, const double *A, int lda, double rho,
                   double *Q, int ldq, double *Ahat_out, int ldah,
                   double *hist, int hist_cap, orc_result *res);
 
+/* eigenvectors of an upper triangular T (TREVC); X := Q X if Q != NULL */
+void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double *X, int ldx);
+
 #ifdef __cplusplus
 }
 #endif

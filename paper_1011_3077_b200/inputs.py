@@ -283,3 +283,23 @@ def svd_known(m: int, n: int, seed: int, vseed: int, device=None):
     gv = torch.Generator(device=device).manual_seed(vseed)
     V = haar(torch.randn((m + n, m + n), dtype=torch.float64, device=device, generator=gv), device)
     return _finish(A, device), _finish(V, device), U, s, W
+
+
+# ---------------------------------------------------------------------------------------
+# TREVC input: real upper triangular T with
+# distinct real eigenvalues T_ii ~ U[-2, 2] and strictly-upper entries ~ N(0, 1/n^2)
+# (departure from normality ||N||_F ~ 0.7, so X stays far from overflow at n = 16384).
+# ---------------------------------------------------------------------------------------
+def tri_known(n: int, seed: int, device=None):
+    """-> T (n x n upper triangular)."""
+    g = np.random.default_rng(seed)
+    d = g.uniform(-2.0, 2.0, n)
+    if device is None or str(device) == "cpu":
+        T = np.triu(g.standard_normal((n, n)) / n, 1)
+        T[np.arange(n), np.arange(n)] = d
+        return _finish(T, None)
+    import torch
+    gt = torch.Generator(device=device).manual_seed(seed)
+    T = torch.triu(torch.randn((n, n), dtype=torch.float64, device=device, generator=gt) / n, 1)
+    T += torch.diag(torch.as_tensor(d, dtype=torch.float64, device=device))
+    return _finish(T, device)
