@@ -141,6 +141,25 @@ int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, in
                   const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
                   int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
 
+/* Eigenvectors of an upper triangular matrix (TREVC):
+ * X upper triangular with X_jj = 1 and TX = XD, D = diag(T), or, when
+ * Q != NULL, the eigenvectors Q X of A = Q T Q^T.  Real T with real
+ * eigenvalues (the triangular case of the paper; 2x2 blocks of a real quasi-triangular
+ * Schur form are not supported).  No overflow scaling: X_ij grows with the departure from
+ * normality over eigenvalue gaps; a gap below smin = max(2^-52 |T_jj|, DBL_MIN n 2^52) is
+ * replaced by smin (LAPACK dtrevc rule, reading Q19).
+ *  1 h          handle, n <= n_max
+ *  2 stream
+ *  3 n          order >= 1
+ *  4 T, 5 ldt   upper triangular input (device; the strictly lower part is not read)
+ *  6 Q, 7 ldq   optional orthogonal n x n (device) or NULL
+ *  8 X, 9 ldx   out (device) n x n; must not alias T or Q
+ * Blocked (b = 64) as Alg. 8 with block rows swept bottom-up: one DMMA GEMM
+ * S = T[i, i+1:] X[i+1:, i+1:] per block row (n^3/3 flops; + 2 n^3 / 2 for Q X) and one
+ * shifted-block-solve launch.  Enqueued on `stream`; does not synchronise. */
+int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, const double* Q,
+              int ldq, double* X, int ldx);
+
 /* Same step with HOST matrices (column-major, tightly packed ld = n): copies A, B, V, VL to
  * the device, runs sdc_split, and copies Q (and QL, Ahat when non-NULL) back -- the
  * end-to-end path of the public API.  Host buffers may be pageable or pinned. */
@@ -187,7 +206,8 @@ enum { SDC_PROF_GEMM = 0,        /* every DMMA GEMM launch                      
        SDC_PROF_GEMM_W0 = 4,     /* subset of GEMM: split-K W0 = Y^T C of WY applications    */
        SDC_PROF_GEMM_UPD = 5,    /* subset of GEMM: rank-nb updates C -= Y W                 */
        SDC_PROF_GEMM_OTHER = 6,  /* subset of GEMM: the n x n products (a5, a7, a8)         */
-       SDC_PROF_CLASSES = 7 };
+       SDC_PROF_TREVC = 7,       /* sdc_trevc shifted block solves (bytes: T block + column) */
+       SDC_PROF_CLASSES = 8 };
 int sdc_profile(sdc_handle* h, int enable);
 int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, double* work);
 

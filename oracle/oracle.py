@@ -77,6 +77,7 @@ def lib():
                 "orc_grurv_right": [I, P, I, P, I, P, I, P, I, P, P],
                 "orc_grurv_left": [I, P, I, P, I, P, I, P, I],
                 "orc_trevc": [I, P, I, P, I, P, I],
+                "orc_trevc_cols": [I, P, I, I, I, P, I],
             }.items():
                 f = getattr(_lib, name)
                 f.restype = None
@@ -288,3 +289,12 @@ def trevc(T, Q=None):
     X = np.zeros((n, n), order="F")
     lib().orc_trevc(n, _p(T), n, _p(Qf), n, _p(X), n)
     return X
+
+
+def trevc_cols(T, j0, j1):
+    """Columns j0..j1-1 of TREVC's X (n x (j1-j0)), same arithmetic as trevc."""
+    T = _f(T)
+    n = T.shape[0]
+    X = np.zeros((n, n), order="F")
+    lib().orc_trevc_cols(n, _p(T), n, int(j0), int(j1), _p(X), n)
+    return X[:, j0:j1]

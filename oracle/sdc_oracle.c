@@ -603,22 +603,29 @@ int orc_svd_split(int m, int n, const double *A, int lda, double rho,
  * denominator T_ii - T_jj is replaced by smin, i.e. X_ij = -(numerator) / smin, with
  * ulp = 2^-52 and smlnum = DBL_MIN n / ulp.  If Q != NULL the eigenvectors of
  * A = Q T Q^T are returned instead: X := Q X. */
-void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double *X, int ldx) {
+/* columns j0 <= j < j1 of X (column j depends on T(0:j, 0:j) only); X is n x n, the other
+ * columns are not touched */
+void orc_trevc_cols(int n, const double *T, int ldt, int j0, int j1, double *Xt, int ldx) {
   const double ulp = 2.220446049250313e-16, smlnum = 2.2250738585072014e-308 * (double)n / ulp;
-  double *Xt = (double *)calloc((size_t)n * n, sizeof(double));
-#pragma omp parallel for schedule(static) if ((long)n * n >= ORC_PAR_MIN)
-  for (int j = 0; j < n; ++j) {
+#pragma omp parallel for schedule(static) if ((long)n * (j1 - j0) >= ORC_PAR_MIN)
+  for (int j = j0; j < j1; ++j) {
+    for (int i = j + 1; i < n; ++i) EL(Xt, i, j, ldx) = 0.0;
     const double d = EL(T, j, j, ldt);
     const double smin = fmax(ulp * fabs(d), smlnum);
-    EL(Xt, j, j, n) = 1.0;
+    EL(Xt, j, j, ldx) = 1.0;
     for (int i = j - 1; i >= 0; --i) {
-      double num = EL(T, i, j, ldt) * EL(Xt, j, j, n);
-      for (int k = i + 1; k <= j - 1; ++k) num += EL(T, i, k, ldt) * EL(Xt, k, j, n);
+      double num = EL(T, i, j, ldt) * EL(Xt, j, j, ldx);
+      for (int k = i + 1; k <= j - 1; ++k) num += EL(T, i, k, ldt) * EL(Xt, k, j, ldx);
       double den = EL(T, i, i, ldt) - d;               /* (T_ii - T_jj) x = -num */
       if (fabs(den) < smin) den = smin;
-      EL(Xt, i, j, n) = -num / den;
+      EL(Xt, i, j, ldx) = -num / den;
     }
   }
+}
+
+void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double *X, int ldx) {
+  double *Xt = (double *)calloc((size_t)n * n, sizeof(double));
+  orc_trevc_cols(n, T, ldt, 0, n, Xt, n);
   if (Q) {
     orc_gemm(0, 0, n, n, n, Q, ldq, Xt, n, X, ldx);
   } else {

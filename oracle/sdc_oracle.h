@@ -67,6 +67,8 @@ int orc_svd_split(int m, int n, const double *A, int lda, double rho,
 
 /* eigenvectors of an upper triangular T (TREVC); X := Q X if Q != NULL */
 void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double *X, int ldx);
+/* columns j0..j1-1 only (column j depends on T(0:j, 0:j)); the sampled full-size check */
+void orc_trevc_cols(int n, const double *T, int ldt, int j0, int j1, double *X, int ldx);
 
 #ifdef __cplusplus
 }

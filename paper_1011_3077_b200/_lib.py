@@ -31,6 +31,7 @@ _SIGS = {
                       ctypes.POINTER(SdcResult)]),
     "sdc_split_region": (I, [P, P, I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I, P, I, P, I,
                              ctypes.POINTER(SdcResult)]),
+    "sdc_trevc": (I, [P, P, I, P, I, P, I, P, I]),
     "sdc_svd_split": (I, [P, P, I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,
                           ctypes.POINTER(SdcResult)]),
     "sdc_split_host": (I, [P, P, I, P, P, P, P, I, D, I, P, P, P, P, I, ctypes.POINTER(SdcResult)]),

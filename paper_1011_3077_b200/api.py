@@ -157,6 +157,19 @@ class Handle:
         return Q, Ah, SplitInfo(res.k, res.r, res.metric, res.metric_fro, res.iters, res.converged,
                                 res.status, hist)
 
+    def trevc(self, T, Q=None, X=None):
+        """sdc_trevc: eigenvectors X (X_jj = 1, TX = XD) of the upper triangular T, or Q X
+        when Q is given.  Enqueued on the current stream."""
+        n = T.shape[0]
+        T = colmajor(T)
+        Q = None if Q is None else colmajor(Q)
+        X = empty_colmajor(n, n, T.device) if X is None else X
+        pt, lt = _ptr_ld(T)
+        pq, lq = _ptr_ld(Q)
+        px, lx = _ptr_ld(X)
+        check(self.lib.sdc_trevc(self._h, _stream(T.device), n, pt, lt, pq, lq, px, lx), "sdc_trevc")
+        return X
+
     def split_host(self, A: np.ndarray, B=None, V=None, VL=None, max_iters=12, tol=0.0,
                    stop="fixed", Q=None, QL=None, want_ahat=False, stream=None):
         """sdc_split_host on host (numpy, Fortran-ordered fp64) buffers: the end-to-end path."""

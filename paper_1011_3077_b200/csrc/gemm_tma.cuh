@@ -35,6 +35,8 @@ struct TmaGemmArgs {
   int kchunk;             // K per z-slice (multiple of 16)
   long long c_zstride;    // element stride between z-slices of C
   int red_ok;             // RED tiles: C += alpha A^T B may use bulk reduce-add (host-checked)
+  int kupper;             // B_s upper triangular (B_s(k, n) = 0 for k > n): a tile's K loop
+                          // stops at its last column (skips products with zeros only)
 };
 
 // CPRE: the C tile (beta != 0) is brought into shared memory by TMA at kernel start, in
@@ -119,7 +121,7 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   }
   const int m0 = bx * T::BM, n0 = by * T::BN;
   const int kbeg = blockIdx.z * g.kchunk;
-  const int kend = min(g.K, kbeg + g.kchunk);
+  const int kend = min(g.kupper ? min(g.K, n0 + T::BN) : g.K, kbeg + g.kchunk);
   const int ktiles = kend > kbeg ? (kend - kbeg + T::BK - 1) / T::BK : 0;
 
   if (threadIdx.x == 0) {
@@ -283,8 +285,8 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
     m0 = (first + (pid % width) % gs) * T::BM;
     n0 = ((pid % width) / gs) * T::BN;
   };
-  auto ktiles_of = [&](int z) {
-    const int kb = z * g.kchunk, ke = min(g.K, kb + g.kchunk);
+  auto ktiles_of = [&](int z, int n0) {
+    const int kb = z * g.kchunk, ke = min(g.kupper ? min(g.K, n0 + T::BN) : g.K, kb + g.kchunk);
     return ke > kb ? (ke - kb + T::BK - 1) / T::BK : 0;
   };
 
@@ -304,7 +306,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
   if (producer && p_tile < ntiles) {
     int z;
     decode(p_tile, p_m0, p_n0, z);
-    p_nk = ktiles_of(z);
+    p_nk = ktiles_of(z, p_n0);
     p_kb = z * g.kchunk;
   }
   auto issue_next = [&]() {
@@ -314,7 +316,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
       if (p_tile < ntiles) {
         int z;
         decode(p_tile, p_m0, p_n0, z);
-        p_nk = ktiles_of(z);
+        p_nk = ktiles_of(z, p_n0);
         p_kb = z * g.kchunk;
       }
     }
@@ -344,7 +346,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
     int m0, n0, z;
     decode(t, m0, n0, z);
-    const int nk = ktiles_of(z);
+    const int nk = ktiles_of(z, n0);
     double* __restrict__ C = g.C + (long long)z * g.c_zstride;
     if (g.beta != 0.0 && !red) {   // warm L2 with this tile's C while its K loop runs
       constexpr int LPC = (T::BM * 8 + 127) / 128;

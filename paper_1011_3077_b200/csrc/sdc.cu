@@ -28,6 +28,7 @@
 #include "gemm.cuh"
 #include "gemm_tma.cuh"
 #include "panel.cuh"
+#include "trevc.cuh"
 
 using namespace sdc;
 
@@ -279,6 +280,15 @@ bool make_tmap(CUtensorMap* tm, const double* ptr, int rows, int cols, long long
   return r == CUDA_SUCCESS;
 }
 
+// algorithmic flops of a TMA GEMM launch: 2 M N K, or with kupper (B_s upper triangular,
+// zero products skipped) 2 M sum_{c < N} min(K, c + 1)
+double tma_gemm_work(const TmaGemmArgs& g) {
+  const double M = g.M, N = g.N, K = g.K;
+  if (!g.kupper) return 2.0 * M * N * K;
+  const double cols = K >= N ? N * (N + 1) / 2 : K * (K + 1) / 2 + (N - K) * K;
+  return 2.0 * M * cols;
+}
+
 int gemm_variant_override() {
   static int v = -2;
   if (v == -2) {
@@ -311,7 +321,7 @@ int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B,
     tC = tA;
   }
   dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
-  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
+  ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
   gemm_tn_tma_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, tC, g);
   SDC_LAUNCHED(h);
   return 0;
@@ -333,7 +343,7 @@ int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const doub
   }
   const long long tiles = (long long)cdiv(g.M, T::BM) * cdiv(g.N, T::BN) * splits;
   const int grid = (int)std::min<long long>(tiles, (long long)h->num_sms * T::MINB);
-  ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
+  ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
   gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, g);
   SDC_LAUNCHED(h);
   return 0;
@@ -362,13 +372,13 @@ int persist_mode() {
 int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, long long lda,
             const double* B, long long ldb, double beta, double* C, long long ldc,
             double* D2 = nullptr, long long ldd2 = 0, double alpha2 = 0.0, int splits = 1,
-            int kchunk = 0, long long c_zstride = 0) {
+            int kchunk = 0, long long c_zstride = 0, int kupper = 0) {
   if (M <= 0 || N <= 0) return 0;
   if (splits <= 1) { splits = 1; kchunk = std::max(K, 1); }
   const bool tma = K > 0 && al16(A, lda) && al16(B, ldb) && tma_encode_fn() != nullptr;
   if (tma) {
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
-                  (int)(al16(C, ldc) && M % 2 == 0)};
+                  (int)(al16(C, ldc) && M % 2 == 0), kupper};
     int v = gemm_variant_override();
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
@@ -1140,6 +1150,49 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
   if (region != SDC_REGION_UNIT_DISK) { set_err("sdc_split: use sdc_split_region for region %d", region); return -12; }
   return sdc_split_region(h, stream, n, A, lda, B, ldb, V, ldv, VL, ldvl, region, 1.0, 0, max_iters,
                           tol, stop_mode, Q, ldq, QL, ldql, Ahat, ldah, hist, hist_cap, res);
+}
+
+int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, const double* Q,
+              int ldq, double* X, int ldx) {
+  SDC_TRY(check_handle(h));
+  if (n < 1 || n > h->n_max) { set_err("n=%d outside [1, n_max=%d]", n, h->n_max); return -3; }
+  if (!T) { set_err("T is NULL"); return -4; }
+  if (ldt < n) { set_err("ldt < n"); return -5; }
+  if (Q && ldq < n) { set_err("ldq < n"); return -7; }
+  if (!X) { set_err("X is NULL"); return -8; }
+  if (ldx < n) { set_err("ldx < n"); return -9; }
+  h->st = static_cast<cudaStream_t>(stream);
+  double* Xw = Q ? h->G2 : X;                  // X_T (the eigenvectors of T)
+  const long long ldw = Q ? n : ldx;
+  SDC_CK(cudaMemset2DAsync(Xw, ldw * sizeof(double), 0, (size_t)n * sizeof(double), n, h->st));
+  double* Tt = h->G1;                          // T^T: K-major A operand of S = T[i,:] X
+  SDC_TRY(transpose_rev(h, Tt, n, T, ldt, n, 0));
+  const int nblk = cdiv(n, TREVC_B);
+  for (int ib = nblk - 1; ib >= 0; --ib) {
+    const int i0 = ib * TREVC_B, nbk = std::min(TREVC_B, n - i0), c0 = i0 + nbk;
+    const int N = n - c0;
+    int splits = 1;
+    if (N > 0) {   // S = T[i0:c0, c0:n] X[c0:n, c0:n]  (X upper triangular: kupper)
+      const int tiles = cdiv(N, 128);
+      splits = pick_splits(h, tiles, N, (long long)(h->wp_elems / ((size_t)TREVC_B * N)));
+      int kchunk = cdiv(cdiv(N, splits), 16) * 16;
+      splits = cdiv(N, kchunk);
+      SDC_TRY(gemm_tn(h, nbk, N, N, 1.0, Tt + c0 + (long long)i0 * n, n, Xw + c0 + (long long)c0 * ldw,
+                      ldw, 0.0, h->Wp, TREVC_B, nullptr, 0, 0.0, splits, kchunk,
+                      (long long)TREVC_B * N, 1));
+    }
+    const int cols = n - i0;
+    ProfScope ps(h, SDC_PROF_TREVC, 8.0 * ((double)nbk * nbk + (double)cols * (nbk * (splits + 1))));
+    k_trevc_block<<<std::min(cdiv(cols, 8), h->num_sms * 8), 256, 0, h->st>>>(
+        T, ldt, i0, nbk, i0, n, h->Wp, splits, (long long)TREVC_B * N, TREVC_B, c0, Xw, ldw, n);
+    SDC_LAUNCHED(h);
+  }
+  if (Q) {   // eigenvectors of A = Q T Q^T: X = Q X_T (TN: A_s = Q^T; X_T upper triangular)
+    double* Qt = h->G3;
+    SDC_TRY(transpose_rev(h, Qt, n, Q, ldq, n, 0));
+    SDC_TRY(gemm_tn(h, n, n, n, 1.0, Qt, n, Xw, ldw, 0.0, X, ldx, nullptr, 0, 0.0, 1, 0, 0, 1));
+  }
+  return 0;
 }
 
 int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, int lda, double rho,

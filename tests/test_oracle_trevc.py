@@ -70,3 +70,10 @@ def test_trevc_repeated_eigenvalue_guard(orc):
     smin = max(ulp * 2.0, np.finfo(float).tiny * 2 / ulp)
     assert np.isfinite(X).all()
     assert X[0, 1] == -1.0 / smin
+
+
+def test_trevc_cols_match_full(orc):
+    T = inputs.tri_known(90, 11)
+    X = orc.trevc(T)
+    for j0, j1 in [(0, 1), (37, 41), (89, 90)]:
+        assert np.array_equal(orc.trevc_cols(T, j0, j1), X[:, j0:j1])
