@@ -59,6 +59,11 @@ def lib():
             _lib.orc_svd_split.restype = I
             _lib.orc_svd_split.argtypes = [I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,
                                            ctypes.POINTER(_Result)]
+            U64 = ctypes.c_ulonglong
+            _lib.orc_haar.restype = None
+            _lib.orc_haar.argtypes = [I, U64, U64, P, I]
+            _lib.orc_schur.restype = I
+            _lib.orc_schur.argtypes = [I, P, I, I, U64, I, D, P, I, P, I, P, P, P, P, P]
             _lib.orc_split_select.restype = D
             _lib.orc_split_select.argtypes = [I, P, I, D, P, I, D, ctypes.POINTER(I), P]
             _lib.orc_norm1.restype = D
@@ -298,3 +303,44 @@ def trevc_cols(T, j0, j1):
     X = np.zeros((n, n), order="F")
     lib().orc_trevc_cols(n, _p(T), n, int(j0), int(j1), _p(X), n)
     return X[:, j0:j1]
+
+
+def haar_stream(m, seed, key):
+    """Haar V of order m from the counter-based Gaussian stream (seed, key)."""
+    V = np.zeros((m, m), order="F")
+    lib().orc_haar(int(m), int(seed), int(key), _p(V), int(m))
+    return V
+
+
+@dataclass
+class SchurResult:
+    Q: np.ndarray
+    T: np.ndarray
+    blocks: list          # [(offset, size)] in processing order
+    splits: int
+    failed_attempts: int
+    unsplit: int
+    passes: int
+    max_metric: float
+
+
+def schur(A, leaf=1, seed=1, max_iters=60, tol=1e-13) -> SchurResult:
+    """Recursive divide-and-conquer A = Q T Q^T, T block upper triangular."""
+    A = _f(A)
+    n = A.shape[0]
+    Q = np.zeros((n, n), order="F")
+    T = np.zeros((n, n), order="F")
+    off = np.zeros(n, dtype=np.int32)
+    size = np.zeros(n, dtype=np.int32)
+    nb = ctypes.c_int(0)
+    stats = np.zeros(4, dtype=np.int32)
+    mm = ctypes.c_double(0.0)
+    rc = lib().orc_schur(n, _p(A), n, int(leaf), int(seed), int(max_iters), float(tol), _p(Q), n,
+                         _p(T), n, off.ctypes.data_as(ctypes.c_void_p),
+                         size.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nb),
+                         stats.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mm))
+    if rc != 0:
+        raise ValueError(f"orc_schur returned {rc}")
+    blocks = [(int(off[i]), int(size[i])) for i in range(nb.value)]
+    return SchurResult(Q, T, blocks, int(stats[0]), int(stats[1]), int(stats[2]), int(stats[3]),
+                       mm.value)

@@ -29,6 +29,7 @@
 #include "sdc_oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -633,4 +634,140 @@ void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double
       for (int i = 0; i < n; ++i) EL(X, i, j, ldx) = EL(Xt, i, j, n);
   }
   free(Xt);
+}
+
+/* ---------------------------------------------------------------------------------------
+ * Recursive divide-and-conquer ("zero out E21 and
+ * recurse on A11, A22", random splitting lines PAPER.md:472-475, 545).  Real arithmetic:
+ * the lines are vertical, Re z = a (theta in {0, pi}), mapped to the unit circle through
+ * the Moebius pencil (A - (a-1)I, A - (a+1)I) (orc_split_region HALFPLANE).  The
+ * decisions follow DESIGN.md §10 "recursion" exactly, shared with sdc_schur:
+ *   - block (o, m) with m <= leaf, or m == 2 with complex eigenvalues: a leaf;
+ *   - real-part Gershgorin interval [lo, hi] of the block (rows, "e.g. using
+ *     Gershgorin bounds"); lo == hi: unsplittable leaf;
+ *   - attempt t (t < 8): a = lo + (0.25 + 0.5 u)(hi - lo), u = U01(seed, 2 s), V = Haar of
+ *     order m from the Gaussian stream 2 s + 1 (s = running split counter); RNEP step in
+ *     monitor mode (stop at the first pass with ||E21||_1/||A||_1 <= tol) with
+ *     at most max_iters passes; accepted iff status 0 (metric <= 1e-8, reading Q4);
+ *   - accepted: T(o:o+m, o:o+m) = Ahat with E21 := 0, T(o:o+m, o+m:n) = Qb^T T(...),
+ *     T(0:o, o:o+m) = T(...) Qb, Q(:, o:o+m) = Q(...) Qb; children (o, r) then (o+r, m-r)
+ *     (processed depth first, leading block first);
+ *   - 8 failed attempts: an unsplit leaf.
+ * Counter-based generator (splitmix64) so both sides draw the same numbers. */
+static uint64_t orc_mix64(uint64_t seed, uint64_t ctr) {
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull * (ctr + 1ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static double orc_u01(uint64_t seed, uint64_t ctr) {
+  return (double)(orc_mix64(seed, ctr) >> 11) * 1.1102230246251565e-16;   /* [0, 1) */
+}
+/* Gaussian (Box-Muller) entry (i, j) of the order-m matrix of stream `key` */
+static double orc_gauss(uint64_t seed, uint64_t key, int m, int i, int j) {
+  const uint64_t base = (key << 40) + 2ull * ((uint64_t)i + (uint64_t)j * (uint64_t)m);
+  const double u1 = (double)((orc_mix64(seed, base) >> 11) + 1ull) * 1.1102230246251565e-16;  /* (0,1] */
+  const double u2 = orc_u01(seed, base + 1ull);
+  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+void orc_haar(int m, unsigned long long seed, unsigned long long key, double *V, int ldv) {
+  double *G = (double *)malloc(sizeof(double) * (size_t)m * m), *tau = (double *)malloc(sizeof(double) * m);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) EL(G, i, j, m) = orc_gauss(seed, key, m, i, j);
+  orc_geqr2(m, m, G, m, tau);
+  orc_org2r_signed(m, G, m, tau, V, ldv);
+  free(G);
+  free(tau);
+}
+
+int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed, int max_iters, double tol,
+              double *Q, int ldq, double *T, int ldt, int *blk_off, int *blk_size, int *nblk,
+              int *stats, double *max_metric) {
+  if (n < 1 || lda < n || ldq < n || ldt < n || leaf < 1) return -1;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      EL(T, i, j, ldt) = EL(A, i, j, lda);
+      EL(Q, i, j, ldq) = i == j ? 1.0 : 0.0;
+    }
+  for (int q = 0; q < 4; ++q) stats[q] = 0;   /* splits, failed attempts, unsplit leaves, passes */
+  *max_metric = 0.0;                           /* largest accepted ||E21||_1/||A_blk||_1 */
+  int *st_o = (int *)malloc(sizeof(int) * 2 * n), *st_m = (int *)malloc(sizeof(int) * 2 * n);
+  int sp = 0, nb = 0;
+  uint64_t s = 0;
+  st_o[sp] = 0; st_m[sp] = n; ++sp;
+  double *Tb = (double *)malloc(sizeof(double) * (size_t)n * n);
+  double *V = (double *)malloc(sizeof(double) * (size_t)n * n);
+  double *Qb = (double *)malloc(sizeof(double) * (size_t)n * n);
+  double *Ab = (double *)malloc(sizeof(double) * (size_t)n * n);
+  double *W = (double *)malloc(sizeof(double) * (size_t)n * n);
+  while (sp > 0) {
+    --sp;
+    const int o = st_o[sp], m = st_m[sp];
+    int leafy = m <= leaf;
+    if (!leafy && m == 2) {   /* 2x2 with complex eigenvalues: a standardised leaf */
+      const double a = EL(T, o, o, ldt), b = EL(T, o, o + 1, ldt), c = EL(T, o + 1, o, ldt),
+                   d = EL(T, o + 1, o + 1, ldt);
+      if ((a - d) * (a - d) + 4.0 * b * c < 0.0) leafy = 1;
+    }
+    double lo = INFINITY, hi = -INFINITY;
+    if (!leafy) {
+      for (int i = 0; i < m; ++i) {
+        double r = 0.0;
+        for (int j = 0; j < m; ++j)
+          if (j != i) r += fabs(EL(T, o + i, o + j, ldt));
+        const double t = EL(T, o + i, o + i, ldt);
+        lo = fmin(lo, t - r);
+        hi = fmax(hi, t + r);
+      }
+      if (!(hi > lo)) { leafy = 1; stats[2]++; }
+    }
+    int done = 0;
+    for (int att = 0; !leafy && att < 8; ++att) {
+      const double u = orc_u01(seed, 2ull * s);
+      const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
+      orc_haar(m, seed, 2ull * s + 1ull, V, m);
+      ++s;
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) EL(Tb, i, j, m) = EL(T, o + i, o + j, ldt);
+      orc_result res;
+      int rc = orc_split_region(m, Tb, m, NULL, 0, V, m, NULL, 0, ORC_REGION_HALFPLANE, a, 0,
+                                max_iters, tol, ORC_STOP_E21, Qb, m, NULL, 0, Ab, m, NULL, 0, &res);
+      if (rc) { free(st_o); free(st_m); free(Tb); free(V); free(Qb); free(Ab); free(W); return rc; }
+      stats[3] += res.iters;
+      if (res.status != ORC_STATUS_SPLIT) { stats[1]++; continue; }
+      const int r = res.r;
+      stats[0]++;
+      *max_metric = fmax(*max_metric, res.metric);
+      /* T(o:o+m, o:o+m) = Ahat with E21 = 0 */
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) EL(T, o + i, o + j, ldt) = (i >= r && j < r) ? 0.0 : EL(Ab, i, j, m);
+      /* T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n) */
+      const int nr = n - o - m;
+      if (nr > 0) {
+        orc_gemm(1, 0, m, nr, m, Qb, m, &EL(T, o, o + m, ldt), ldt, W, m);
+        for (int j = 0; j < nr; ++j)
+          for (int i = 0; i < m; ++i) EL(T, o + i, o + m + j, ldt) = EL(W, i, j, m);
+      }
+      /* T(0:o, o:o+m) = T(0:o, o:o+m) Qb */
+      if (o > 0) {
+        orc_gemm(0, 0, o, m, m, &EL(T, 0, o, ldt), ldt, Qb, m, W, o);
+        for (int j = 0; j < m; ++j)
+          for (int i = 0; i < o; ++i) EL(T, i, o + j, ldt) = EL(W, i, j, o);
+      }
+      /* Q(:, o:o+m) = Q(:, o:o+m) Qb */
+      orc_gemm(0, 0, n, m, m, &EL(Q, 0, o, ldq), ldq, Qb, m, W, n);
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < n; ++i) EL(Q, i, o + j, ldq) = EL(W, i, j, n);
+      st_o[sp] = o + r; st_m[sp] = m - r; ++sp;   /* trailing (Re < a), processed second */
+      st_o[sp] = o; st_m[sp] = r; ++sp;           /* leading (Re > a), processed first   */
+      done = 1;
+      break;
+    }
+    if (!leafy && !done) stats[2]++;
+    if (leafy || !done) { blk_off[nb] = o; blk_size[nb] = m; ++nb; }
+  }
+  *nblk = nb;
+  free(st_o); free(st_m); free(Tb); free(V); free(Qb); free(Ab); free(W);
+  return 0;
 }

@@ -70,6 +70,13 @@ void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double
 /* columns j0..j1-1 only (column j depends on T(0:j, 0:j)); the sampled full-size check */
 void orc_trevc_cols(int n, const double *T, int ldt, int j0, int j1, double *X, int ldx);
 
+/* Haar orthogonal V of order m from the counter-based Gaussian stream `key` (QR, diag R >= 0) */
+void orc_haar(int m, unsigned long long seed, unsigned long long key, double *V, int ldv);
+/* recursive divide-and-conquer to block upper triangular form A = Q T Q^T */
+int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed, int max_iters,
+              double tol, double *Q, int ldq, double *T, int ldt, int *blk_off, int *blk_size,
+              int *nblk, int *stats, double *max_metric);
+
 #ifdef __cplusplus
 }
 #endif
