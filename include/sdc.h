@@ -60,8 +60,12 @@ enum {
                                pencil (A-(a-1)I, A-(a+1)I); Q^T A Q of the
                                original A, single right subspace                             */
 };
-enum { SDC_FLAG_SYMMETRIC = 1 /* RSEP, Alg. 6: Ahat <- (Ahat + Ahat^T)/2
-                                 before the split selection; B = I only                     */ };
+enum { SDC_FLAG_SYMMETRIC = 1, /* RSEP, Alg. 6: Ahat <- (Ahat + Ahat^T)/2
+                                  before the split selection; B = I only                     */
+       SDC_FLAG_PLATEAU = 2,   /* SDC_STOP_E21 only: also stop once the metric is <= 10 tol and
+                                  no longer halves (the rounding floor)       */
+       SDC_FLAG_ONESIDED = 4   /* SDC_STOP_E21 only: stop after pass >= 3 once res.side is within
+                                  1e-6 of 0 or 1 (no eigenvalue on one side of the boundary) */ };
 enum { SDC_STATUS_SPLIT = 0, SDC_STATUS_NO_SPLIT = 1, SDC_STATUS_NONFINITE = 2 };
 #define SDC_SPLIT_ACCEPT 1e-8 /* status 0 iff metric <= this (reading Q4)       */
 
@@ -73,6 +77,10 @@ typedef struct {
   int iters;         /* IRS passes executed (p)                                            */
   int converged;     /* 1 if the RTEST/E21 stop rule fired before max_iters                 */
   int status;        /* SDC_STATUS_*                                                       */
+  double side;       /* ||B_p||_F / (||A_p||_F + ||B_p||_F) of the final right IRS pair:
+                        -> 0 when every eigenvalue is outside the region, -> 1 when every one
+                        is inside (A_p^{-1} B_p = (A^{-1} B)^{2^p}); used by
+                        sdc_schur to move its line after a one-sided step */
 } sdc_result;
 
 typedef struct sdc_handle sdc_handle;
@@ -140,6 +148,33 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
 int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, int lda, double rho,
                   const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
                   int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
+
+/* Recursive divide-and-conquer to block upper triangular form A = Q T Q^T (
+ * PAPER.md:406-410 "zero E21 and recurse on (A11, A22)", random splitting lines
+ * PAPER.md:472-475 restricted to real arithmetic: vertical lines Re z = a).
+ * Decisions (DESIGN.md §10 "recursion", identical in orc_schur): a block of order m is a leaf
+ * if m <= leaf, or m == 2 with complex eigenvalues; else up to 16 attempts, each a random
+ * line in the middle half of [c - 2s, c + 2s] (c = trace/m, s = ||T_blk - cI||_F/sqrt(m)),
+ * a counter-based Haar V (seed), and one RNEP half-plane step in monitor mode
+ * (SDC_STOP_E21 with `tol`, at most max_iters passes), accepted iff its status is 0; a
+ * rejected step whose res.side shows every eigenvalue on one side moves that end of the
+ * interval to the line.  On acceptance E21 := 0,
+ * T and Q are updated by the block's Q_b and the two diagonal blocks are processed depth
+ * first (eigenvalues right of the line first).  16 failed attempts: an unsplit leaf.
+ *  1 h, 2 stream, 3 n (<= n_max), 4 A, 5 lda (device input)
+ *  6 leaf        >= 1: largest diagonal block left unsplit (1: real Schur-like form)
+ *  7 seed        generator seed (lines and Haar matrices)
+ *  8 max_iters, 9 tol   per split (monitor mode)
+ * 10 Q, 11 ldq  out (device): orthogonal n x n
+ * 12 T, 13 ldt  out (device): block upper triangular, exactly 0 below the diagonal blocks
+ * 14 blk_off, 15 blk_size   HOST out (n ints each): the diagonal blocks, processing order
+ * 16 nblk       HOST out: number of blocks
+ * 17 stats      HOST out (4 ints): accepted splits, failed attempts, unsplit leaves, passes
+ * 18 max_metric HOST out: largest accepted ||E21||_1/||A_block||_1 (the backward error per split)
+ * Allocates 5 n x n scratch matrices for the duration of the call; synchronises `stream`. */
+int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int leaf,
+              unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
+              int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric);
 
 /* Eigenvectors of an upper triangular matrix (TREVC):
  * X upper triangular with X_jj = 1 and TX = XD, D = diag(T), or, when

@@ -21,7 +21,7 @@ _lib = None
 
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
 REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
-FLAG_SYMMETRIC = 1
+FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED = 1, 2, 4
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
 SPLIT_ACCEPT = 1e-8
 
@@ -41,7 +41,7 @@ def build(force: bool = False) -> str:
 class _Result(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int), ("r", ctypes.c_int), ("metric", ctypes.c_double),
                 ("metric_fro", ctypes.c_double), ("iters", ctypes.c_int),
-                ("converged", ctypes.c_int), ("status", ctypes.c_int)]
+                ("converged", ctypes.c_int), ("status", ctypes.c_int), ("side", ctypes.c_double)]
 
 
 def lib():

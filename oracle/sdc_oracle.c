@@ -478,6 +478,7 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   if (region < 0 || region > 2) return -30;
   if (region == ORC_REGION_DISK && !(param > 0.0)) return -31;
   if ((region == ORC_REGION_HALFPLANE || (flags & ORC_FLAG_SYMMETRIC)) && B) return -32;
+  if (flags & ~(ORC_FLAG_SYMMETRIC | ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED)) return -33;
   const int sym = (flags & ORC_FLAG_SYMMETRIC) != 0;
   const double rho = region == ORC_REGION_DISK ? param : 1.0;
   if (n < 2) return -1;
@@ -517,11 +518,18 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   for (int i = 0; i < hist_cap * 3 && hist; ++i) hist[i] = NAN;
 
   int p = max_iters, conv = 0, r = 1;
-  double met = INFINITY, mfro = INFINITY;
+  double met = INFINITY, mfro = INFINITY, prev = INFINITY;
   int have_split = 0;
   for (int j = 0; j < max_iters; ++j) {
     orc_irs_pass(n, Aj, n, Bj, n, Aj, n, Bj, n, Rc);
     if (pencil) orc_irs_pass(n, Lj, n, Mj, n, Lj, n, Mj, n, NULL);
+    if ((flags & ORC_FLAG_ONESIDED) && stop_mode == ORC_STOP_E21 && j >= 2) {
+      /* every eigenvalue on one side: (A^{-1}B)^{2^p} -> 0 or infinity, one of A_p, B_p
+       * vanishes relative to the other -- no split exists, stop */
+      const double fa = norm_fro(n, n, Aj, n), fb = norm_fro(n, n, Bj, n);
+      const double sd = fa + fb > 0.0 ? fb / (fa + fb) : 0.5;
+      if (sd < 1e-6 || sd > 1.0 - 1e-6) { p = j + 1; break; }
+    }
     double ratio = NAN;
     if (j >= 1) {
       double *D = (double *)malloc(sizeof(double) * nn);
@@ -541,6 +549,11 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
       have_split = 1;
       if (hist && j < hist_cap) { hist[3 * j] = r; hist[3 * j + 1] = met; }
       if (met <= tol) { p = j + 1; conv = 1; break; }
+      /* plateau: a metric within 10 tol that no longer halves -- the rounding floor */
+      if ((flags & ORC_FLAG_PLATEAU) && met <= 10.0 * tol && met > 0.5 * prev) {
+        p = j + 1; conv = 1; break;
+      }
+      prev = met;
     }
   }
   if (!have_split) {
@@ -562,6 +575,10 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   res->metric_fro = mfro;
   res->iters = p;
   res->converged = conv;
+  {   /* side indicator of the final right IRS pair: ||B_p||_F / (||A_p||_F + ||B_p||_F) */
+    const double fa = norm_fro(n, n, Aj, n), fb = norm_fro(n, n, Bj, n);
+    res->side = fa + fb > 0.0 ? fb / (fa + fb) : 0.5;
+  }
   res->status = !all_finite(nn, Ah) || !isfinite(met) ? ORC_STATUS_NONFINITE
               : (met <= ORC_SPLIT_ACCEPT ? ORC_STATUS_SPLIT : ORC_STATUS_NO_SPLIT);
   free(Aj); free(Bj); free(Rp); free(Rc); free(Ah);
@@ -643,16 +660,25 @@ void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double
  * the Moebius pencil (A - (a-1)I, A - (a+1)I) (orc_split_region HALFPLANE).  The
  * decisions follow DESIGN.md §10 "recursion" exactly, shared with sdc_schur:
  *   - block (o, m) with m <= leaf, or m == 2 with complex eigenvalues: a leaf;
- *   - real-part Gershgorin interval [lo, hi] of the block (rows, "e.g. using
- *     Gershgorin bounds"); lo == hi: unsplittable leaf;
- *   - attempt t (t < 8): a = lo + (0.25 + 0.5 u)(hi - lo), u = U01(seed, 2 s), V = Haar of
+ *   - search interval for the line: c = trace/m, s = ||T_blk - c I||_F / sqrt(m) (both
+ *     invariant under orthogonal similarity, so rounding-level basis differences do not
+ *     change decisions), [lo, hi] = [c - 2s, c + 2s] (PAPER.md:472-475 uses a disk of radius
+ *     R/2 around the centre; Gershgorin radii of dense blocks are ~sqrt(m) too wide); s = 0:
+ *     unsplittable leaf;
+ *   - attempt t (t < 16): a = lo + (0.25 + 0.5 u)(hi - lo), u = U01(seed, 2 s), V = Haar of
  *     order m from the Gaussian stream 2 s + 1 (s = running split counter); RNEP step in
- *     monitor mode (stop at the first pass with ||E21||_1/||A||_1 <= tol) with
- *     at most max_iters passes; accepted iff status 0 (metric <= 1e-8, reading Q4);
+ *     monitor mode (stop at the first pass with ||E21||_1/||A||_1 <= tol_b = max(tol, 8e-15 m),
+ *     PAPER.md:597, or at a plateau <= 10 tol_b that no longer halves, or once the IRS pair
+ *     is one-sided) with at most max_iters passes; accepted iff status 0 (<= 1e-8, Q4) and
+ *     the pair is not one-sided (res.side within 1e-6 of 0 or 1); a
+ *     rejected step whose IRS pair shows every eigenvalue on one side of the line
+ *     (res.side > 0.95: all Re < a; < 0.05: all Re > a) moves hi (lo) to a -- the paper's
+ *     "progress without a split" -- otherwise the line hit
+ *     the pseudospectrum and the next attempt draws a new a in the same interval;
  *   - accepted: T(o:o+m, o:o+m) = Ahat with E21 := 0, T(o:o+m, o+m:n) = Qb^T T(...),
  *     T(0:o, o:o+m) = T(...) Qb, Q(:, o:o+m) = Q(...) Qb; children (o, r) then (o+r, m-r)
  *     (processed depth first, leading block first);
- *   - 8 failed attempts: an unsplit leaf.
+ *   - 16 failed attempts: an unsplit leaf.
  * Counter-based generator (splitmix64) so both sides draw the same numbers. */
 static uint64_t orc_mix64(uint64_t seed, uint64_t ctr) {
   uint64_t z = seed + 0x9E3779B97F4A7C15ull * (ctr + 1ull);
@@ -710,20 +736,24 @@ int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed
                    d = EL(T, o + 1, o + 1, ldt);
       if ((a - d) * (a - d) + 4.0 * b * c < 0.0) leafy = 1;
     }
-    double lo = INFINITY, hi = -INFINITY;
+    double lo = 0.0, hi = 0.0;
     if (!leafy) {
-      for (int i = 0; i < m; ++i) {
-        double r = 0.0;
-        for (int j = 0; j < m; ++j)
-          if (j != i) r += fabs(EL(T, o + i, o + j, ldt));
-        const double t = EL(T, o + i, o + i, ldt);
-        lo = fmin(lo, t - r);
-        hi = fmax(hi, t + r);
-      }
-      if (!(hi > lo)) { leafy = 1; stats[2]++; }
+      double tr = 0.0;
+      for (int i = 0; i < m; ++i) tr += EL(T, o + i, o + i, ldt);
+      const double c = tr / m;
+      double f2 = 0.0;
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) {
+          const double t = EL(T, o + i, o + j, ldt) - (i == j ? c : 0.0);
+          f2 += t * t;
+        }
+      const double sd = sqrt(f2 / m);
+      lo = c - 2.0 * sd;
+      hi = c + 2.0 * sd;
+      if (!(sd > 0.0)) { leafy = 1; stats[2]++; }
     }
     int done = 0;
-    for (int att = 0; !leafy && att < 8; ++att) {
+    for (int att = 0; !leafy && att < 16; ++att) {
       const double u = orc_u01(seed, 2ull * s);
       const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
       orc_haar(m, seed, 2ull * s + 1ull, V, m);
@@ -731,11 +761,19 @@ int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed
       for (int j = 0; j < m; ++j)
         for (int i = 0; i < m; ++i) EL(Tb, i, j, m) = EL(T, o + i, o + j, ldt);
       orc_result res;
-      int rc = orc_split_region(m, Tb, m, NULL, 0, V, m, NULL, 0, ORC_REGION_HALFPLANE, a, 0,
-                                max_iters, tol, ORC_STOP_E21, Qb, m, NULL, 0, Ab, m, NULL, 0, &res);
+      const double tolb = fmax(tol, 8e-15 * m);   /* rounding floor grows ~ m eps */
+      int rc = orc_split_region(m, Tb, m, NULL, 0, V, m, NULL, 0, ORC_REGION_HALFPLANE, a,
+                                ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED, max_iters, tolb, ORC_STOP_E21,
+                                Qb, m, NULL, 0, Ab, m, NULL, 0, &res);
       if (rc) { free(st_o); free(st_m); free(Tb); free(V); free(Qb); free(Ab); free(W); return rc; }
       stats[3] += res.iters;
-      if (res.status != ORC_STATUS_SPLIT) { stats[1]++; continue; }
+      const int onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
+      if (res.status != ORC_STATUS_SPLIT || onesided) {   /* a one-sided pair's split is incidental */
+        stats[1]++;
+        if (res.side > 0.95) hi = a;          /* every eigenvalue left of the line  */
+        else if (res.side < 0.05) lo = a;     /* every eigenvalue right of the line */
+        continue;
+      }
       const int r = res.r;
       stats[0]++;
       *max_metric = fmax(*max_metric, res.metric);

@@ -12,7 +12,10 @@ extern "C" {
 
 enum { ORC_STOP_FIXED = 0, ORC_STOP_RTEST = 1, ORC_STOP_E21 = 2 };
 enum { ORC_REGION_UNIT_DISK = 0, ORC_REGION_DISK = 1, ORC_REGION_HALFPLANE = 2 };
-enum { ORC_FLAG_SYMMETRIC = 1 };
+enum { ORC_FLAG_SYMMETRIC = 1,
+       ORC_FLAG_PLATEAU = 2,   /* E21 mode: also stop at a metric <= 10 tol that stopped halving */
+       ORC_FLAG_ONESIDED = 4   /* E21 mode: stop after pass >= 3 once ||B_p||/(||A_p||+||B_p||) is
+                                  within 1e-6 of 0 or 1 (every eigenvalue on one side)       */ };
 enum { ORC_STATUS_SPLIT = 0, ORC_STATUS_NO_SPLIT = 1, ORC_STATUS_NONFINITE = 2 };
 #define ORC_SPLIT_ACCEPT 1e-8 /* split_accept_tol (SPEC.md design decision; Q4) */
 
@@ -24,6 +27,10 @@ typedef struct {
   int iters;         /* IRS passes executed                                   */
   int converged;     /* 1 if the stop rule fired before max_iters             */
   int status;        /* ORC_STATUS_*                                          */
+  double side;       /* ||B_p||_F/(||A_p||_F+||B_p||_F) of the final right IRS pair: -> 0
+                        when every eigenvalue of the (mapped) pencil is outside the unit
+                        circle, -> 1 when every one is inside (A_p^{-1}B_p = (A^{-1}B)^{2^p},
+                        PAPER.md:460); the recursion's one-sided test */
 } orc_result;
 
 void orc_geqr2(int m, int n, double *A, int lda, double *tau);

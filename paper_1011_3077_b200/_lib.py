@@ -10,7 +10,7 @@ LIB_PATH = os.path.join(HERE, "libsdc.so")
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
 REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
-FLAG_SYMMETRIC = 1
+FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED = 1, 2, 4
 PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PROF_GEMM_OTHER = 0, 1, 2, 3, 4, 5, 6
 SPLIT_ACCEPT = 1e-8
 
@@ -18,7 +18,7 @@ SPLIT_ACCEPT = 1e-8
 class SdcResult(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int), ("r", ctypes.c_int), ("metric", ctypes.c_double),
                 ("metric_fro", ctypes.c_double), ("iters", ctypes.c_int),
-                ("converged", ctypes.c_int), ("status", ctypes.c_int)]
+                ("converged", ctypes.c_int), ("status", ctypes.c_int), ("side", ctypes.c_double)]
 
 
 _lib = None
@@ -32,6 +32,8 @@ _SIGS = {
     "sdc_split_region": (I, [P, P, I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I, P, I, P, I,
                              ctypes.POINTER(SdcResult)]),
     "sdc_trevc": (I, [P, P, I, P, I, P, I, P, I]),
+    "sdc_schur": (I, [P, P, I, P, I, I, ctypes.c_ulonglong, I, D, P, I, P, I, P, P,
+                      ctypes.POINTER(I), P, ctypes.POINTER(D)]),
     "sdc_svd_split": (I, [P, P, I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,
                           ctypes.POINTER(SdcResult)]),
     "sdc_split_host": (I, [P, P, I, P, P, P, P, I, D, I, P, P, P, P, I, ctypes.POINTER(SdcResult)]),

@@ -157,6 +157,31 @@ class Handle:
         return Q, Ah, SplitInfo(res.k, res.r, res.metric, res.metric_fro, res.iters, res.converged,
                                 res.status, hist)
 
+    def schur(self, A, leaf=1, seed=1, max_iters=60, tol=1e-13, Q=None, T=None):
+        """sdc_schur: recursive divide-and-conquer A = Q T Q^T.
+        Returns (Q, T, blocks [(offset, size)], stats dict)."""
+        n = A.shape[0]
+        A = colmajor(A)
+        Q = empty_colmajor(n, n, A.device) if Q is None else Q
+        T = empty_colmajor(n, n, A.device) if T is None else T
+        off = np.zeros(n, dtype=np.int32)
+        size = np.zeros(n, dtype=np.int32)
+        nb = ctypes.c_int(0)
+        stats = np.zeros(4, dtype=np.int32)
+        mm = ctypes.c_double(0.0)
+        pa, la = _ptr_ld(A)
+        pq, lq = _ptr_ld(Q)
+        pt, lt = _ptr_ld(T)
+        check(self.lib.sdc_schur(self._h, _stream(A.device), n, pa, la, int(leaf), int(seed),
+                                 int(max_iters), float(tol), pq, lq, pt, lt,
+                                 off.ctypes.data_as(ctypes.c_void_p), size.ctypes.data_as(ctypes.c_void_p),
+                                 ctypes.byref(nb), stats.ctypes.data_as(ctypes.c_void_p),
+                                 ctypes.byref(mm)), "sdc_schur")
+        blocks = [(int(off[i]), int(size[i])) for i in range(nb.value)]
+        info = {"splits": int(stats[0]), "failed_attempts": int(stats[1]), "unsplit": int(stats[2]),
+                "passes": int(stats[3]), "max_metric": mm.value}
+        return Q, T, blocks, info
+
     def trevc(self, T, Q=None, X=None):
         """sdc_trevc: eigenvectors X (X_jj = 1, TX = XD) of the upper triangular T, or Q X
         when Q is given.  Enqueued on the current stream."""

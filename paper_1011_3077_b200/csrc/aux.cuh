@@ -52,6 +52,64 @@ __global__ void k_embed(double* H, const double* A, long long lda, int m, int n)
   }
 }
 
+// ---- recursive divide-and-conquer helpers (sdc_schur, DESIGN.md §10 "recursion") ----------
+// counter-based generator shared (re-implemented) by the oracle: splitmix64 of (seed, ctr)
+SDC_DEV unsigned long long mix64(unsigned long long seed, unsigned long long ctr) {
+  unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (ctr + 1ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// Gaussian (Box-Muller) matrix of order m from stream `key`: entry (i, j) uses counters
+// (key << 40) + 2 (i + j m) and +1
+__global__ void k_gauss(double* G, long long ldg, int m, unsigned long long seed, unsigned long long key) {
+  SDC_FOR_MN(m, m) {
+    const int i = (int)(_e % m), j = (int)(_e / m);
+    const unsigned long long base = (key << 40) + 2ull * ((unsigned long long)i + (unsigned long long)j * m);
+    const double u1 = (double)((mix64(seed, base) >> 11) + 1ull) * 1.1102230246251565e-16;
+    const double u2 = (double)(mix64(seed, base + 1ull) >> 11) * 1.1102230246251565e-16;
+    G[i + (long long)j * ldg] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+  }
+}
+// line search interval of the m x m block (invariant under orthogonal similarity):
+// out[0] = c = trace/m, out[1] = ||T - c I||_F / sqrt(m)  (one CTA, fixed-order reductions)
+__global__ void k_block_scale(const double* T, long long ldt, int m, double* out) {
+  __shared__ double red[256];
+  __shared__ double cs;
+  double t = 0.0;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) t += T[i + (long long)i * ldt];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cs = red[0] / m;
+  __syncthreads();
+  const double c = cs;
+  double f = 0.0;
+  for (long long e = threadIdx.x; e < (long long)m * m; e += blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const double v = T[i + (long long)j * ldt] - (i == j ? c : 0.0);
+    f += v * v;
+  }
+  __syncthreads();
+  red[threadIdx.x] = f;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[0] = c; out[1] = sqrt(red[0] / m); }
+}
+// T block (m x m) <- Ahat with E21 = Ahat(r:m, 0:r) set to zero
+__global__ void k_place_ahat(double* T, long long ldt, const double* Ah, long long ldah, int m, int r) {
+  SDC_FOR_MN(m, m) {
+    const int i = (int)(_e % m), j = (int)(_e / m);
+    T[i + (long long)j * ldt] = (i >= r && j < r) ? 0.0 : Ah[i + (long long)j * ldah];
+  }
+}
+
 // tiled transpose-with-remap:  out(i, j) = s(j) * src(ri(i, j), rj(i, j)) where the mode
 // selects the remap (used for RQ = reversed QR of C^T J and QL = reversed QR of J X J):
 //   mode 0: out(i,j) = src(j, i)                      (transpose)

@@ -58,7 +58,8 @@ void set_err(const char* fmt, ...) {
   } while (0)
 
 constexpr int NB = PANEL_NB;       // panel / WY block width
-constexpr int SCAL_HIST = 8;       // scal[8 + j]: R-test ratio of pass j
+constexpr int SCAL_HIST = 12;      // scal[12 + j]: R-test ratio of pass j; scal[8..11]: norms of
+                                   // the final right IRS pair (1, F) of A_p and of B_p
 constexpr int MAX_HIST = 65536;
 
 }  // namespace
@@ -942,6 +943,8 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
     if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
     SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
   }
+  SDC_TRY(norms(h, h->A[cur], ld, n, h->scal + 8));    // side indicator (res->side)
+  SDC_TRY(norms(h, h->B[cur], ld, n, h->scal + 10));
   SDC_CK(cudaMemsetAsync(h->flag, 0, sizeof(int), h->st));
   k_nonfinite<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->Ah, ld, n, h->flag);
   SDC_LAUNCHED(h);
@@ -1152,6 +1155,140 @@ int sdc_split(sdc_handle* h, void* stream, int n, const double* A, int lda, cons
                           tol, stop_mode, Q, ldq, QL, ldql, Ahat, ldah, hist, hist_cap, res);
 }
 
+// host side of the shared counter-based generator (same constants as mix64 in aux.cuh)
+static unsigned long long host_mix64(unsigned long long seed, unsigned long long ctr) {
+  unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (ctr + 1ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int leaf,
+              unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
+              int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric) {
+  SDC_TRY(check_handle(h));
+  if (n < 1 || n > h->n_max) { set_err("n=%d outside [1, n_max=%d]", n, h->n_max); return -3; }
+  if (!A) { set_err("A is NULL"); return -4; }
+  if (lda < n) { set_err("lda < n"); return -5; }
+  if (leaf < 1) { set_err("leaf < 1"); return -6; }
+  if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -8; }
+  if (!(tol >= 0.0)) { set_err("tol < 0"); return -9; }
+  if (!Q) { set_err("Q is NULL"); return -10; }
+  if (ldq < n) { set_err("ldq < n"); return -11; }
+  if (!T) { set_err("T is NULL"); return -12; }
+  if (ldt < n) { set_err("ldt < n"); return -13; }
+  if (!blk_off || !blk_size || !nblk || !stats || !max_metric) { set_err("NULL host output"); return -14; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->st = st;
+  // workspace of this call: V / Gaussian, Q_b, Ahat_b, product scratch, scalars
+  double *Vb = nullptr, *Gb = nullptr, *Qb = nullptr, *Ab = nullptr, *W = nullptr, *sc = nullptr;
+  const size_t nn = (size_t)n * n;
+  auto cleanup = [&]() {
+    for (double* p : {Vb, Gb, Qb, Ab, W, sc}) if (p) cudaFree(p);
+  };
+  if (cudaMalloc(&Vb, nn * 8) || cudaMalloc(&Gb, nn * 8) || cudaMalloc(&Qb, nn * 8) ||
+      cudaMalloc(&Ab, nn * 8) || cudaMalloc(&W, nn * 8) || cudaMalloc(&sc, 64)) {
+    cleanup();
+    set_err("sdc_schur: out of device memory");
+    return SDC_ERR_NOMEM;
+  }
+  int rc = 0;
+  auto run = [&]() -> int {
+    k_copy<<<ew_grid((long long)nn), 256, 0, st>>>(T, ldt, A, lda, n, n, 1.0);
+    SDC_LAUNCHED(h);
+    k_set_identity<<<ew_grid((long long)nn), 256, 0, st>>>(Q, ldq, n, n, 1.0);
+    SDC_LAUNCHED(h);
+    for (int q = 0; q < 4; ++q) stats[q] = 0;
+    *max_metric = 0.0;
+    std::vector<std::pair<int, int>> stack{{0, n}};
+    int nb = 0;
+    unsigned long long s = 0;
+    double hs[4];
+    while (!stack.empty()) {
+      const int o = stack.back().first, m = stack.back().second;
+      stack.pop_back();
+      bool leafy = m <= leaf;
+      if (!leafy && m == 2) {   // 2x2 with complex eigenvalues: a standardised leaf
+        SDC_CK(cudaMemcpy2DAsync(hs, 2 * sizeof(double), T + o + (long long)o * ldt, ldt * sizeof(double),
+                                 2 * sizeof(double), 2, cudaMemcpyDeviceToHost, st));
+        SDC_CK(cudaStreamSynchronize(st));
+        const double a = hs[0], c = hs[1], b = hs[2], d = hs[3];
+        if ((a - d) * (a - d) + 4.0 * b * c < 0.0) leafy = true;
+      }
+      double lo = 0.0, hi = 0.0;
+      if (!leafy) {   // [c - 2s, c + 2s], c = trace/m, s = ||T_blk - cI||_F / sqrt(m)
+        k_block_scale<<<1, 256, 0, st>>>(T + o + (long long)o * ldt, ldt, m, sc);
+        SDC_LAUNCHED(h);
+        SDC_CK(cudaMemcpyAsync(hs, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SDC_CK(cudaStreamSynchronize(st));
+        lo = hs[0] - 2.0 * hs[1];
+        hi = hs[0] + 2.0 * hs[1];
+        if (!(hs[1] > 0.0)) { leafy = true; stats[2]++; }
+      }
+      bool done = false;
+      for (int att = 0; !leafy && att < 16; ++att) {
+        const double u = (double)(host_mix64(seed, 2ull * s) >> 11) * 1.1102230246251565e-16;
+        const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
+        k_gauss<<<ew_grid((long long)m * m), 256, 0, st>>>(Gb, m, m, seed, 2ull * s + 1ull);
+        SDC_LAUNCHED(h);
+        ++s;
+        SDC_TRY(sdc_qr(h, st, m, m, Gb, m, Vb, m));                 // Haar V (diag R >= 0)
+        sdc_result res;
+        const double tolb = std::max(tol, 8e-15 * m);   // rounding floor grows ~ m eps
+        SDC_TRY(sdc_split_region(h, st, m, T + o + (long long)o * ldt, ldt, nullptr, 0, Vb, m, nullptr, 0,
+                                 SDC_REGION_HALFPLANE, a, SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED,
+                                 max_iters, tolb, SDC_STOP_E21, Qb, m, nullptr, 0, Ab, m, nullptr, 0,
+                                 &res));
+        h->st = st;
+        stats[3] += res.iters;
+        const bool onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
+        if (res.status != 0 || onesided) {   // a one-sided pair's split is incidental
+          stats[1]++;
+          if (res.side > 0.95) hi = a;          // every eigenvalue left of the line
+          else if (res.side < 0.05) lo = a;     // every eigenvalue right of the line
+          continue;
+        }
+        const int r = res.r;
+        stats[0]++;
+        *max_metric = std::max(*max_metric, res.metric);
+        k_place_ahat<<<ew_grid((long long)m * m), 256, 0, st>>>(T + o + (long long)o * ldt, ldt, Ab, m, m, r);
+        SDC_LAUNCHED(h);
+        const int nr = n - o - m;
+        if (nr > 0) {   // T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n)
+          double* Tr = T + o + (long long)(o + m) * ldt;
+          SDC_TRY(gemm_tn(h, m, nr, m, 1.0, Qb, m, Tr, ldt, 0.0, W, m));
+          k_copy<<<ew_grid((long long)m * nr), 256, 0, st>>>(Tr, ldt, W, m, m, nr, 1.0);
+          SDC_LAUNCHED(h);
+        }
+        if (o > 0) {    // T(0:o, o:o+m) = T(0:o, o:o+m) Qb
+          double* Tu = T + (long long)o * ldt;
+          SDC_TRY(gemm_general(h, false, false, o, m, m, 1.0, Tu, ldt, Qb, m, 0.0, W, o));
+          k_copy<<<ew_grid((long long)o * m), 256, 0, st>>>(Tu, ldt, W, o, o, m, 1.0);
+          SDC_LAUNCHED(h);
+        }
+        {               // Q(:, o:o+m) = Q(:, o:o+m) Qb
+          double* Qc = Q + (long long)o * ldq;
+          SDC_TRY(gemm_general(h, false, false, n, m, m, 1.0, Qc, ldq, Qb, m, 0.0, W, n));
+          k_copy<<<ew_grid((long long)n * m), 256, 0, st>>>(Qc, ldq, W, n, n, m, 1.0);
+          SDC_LAUNCHED(h);
+        }
+        stack.push_back({o + r, m - r});   // trailing (Re < a), processed second
+        stack.push_back({o, r});           // leading (Re > a), processed first
+        done = true;
+        break;
+      }
+      if (!leafy && !done) stats[2]++;
+      if (leafy || !done) { blk_off[nb] = o; blk_size[nb] = m; ++nb; }
+    }
+    *nblk = nb;
+    SDC_CK(cudaStreamSynchronize(st));
+    return 0;
+  };
+  rc = run();
+  cleanup();
+  return rc;
+}
+
 int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, const double* Q,
               int ldq, double* X, int ldx) {
   SDC_TRY(check_handle(h));
@@ -1240,7 +1377,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     set_err("half-plane regions and the symmetric flag take B = NULL (B = I)");
     return -6;
   }
-  if (flags & ~SDC_FLAG_SYMMETRIC) { set_err("unknown flags"); return -14; }
+  if (flags & ~(SDC_FLAG_SYMMETRIC | SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED)) { set_err("unknown flags"); return -14; }
   h->region = region;
   h->rparam = region == SDC_REGION_UNIT_DISK ? 1.0 : region_param;
   h->rflags = flags;
@@ -1312,6 +1449,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
     int cur = 0;
     bool have_split = false;
+    double prev = INFINITY;
     for (int j = 0; j < max_iters; ++j) {
       SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S,
                        j, nullptr, 0));
@@ -1319,6 +1457,16 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
         SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
                          h->SL, -1, nullptr, 0));
       cur ^= 1;
+      if ((flags & SDC_FLAG_ONESIDED) && stop_mode == SDC_STOP_E21 && j >= 2) {
+        // every eigenvalue on one side: one of A_p, B_p vanishes relative to the other
+        SDC_TRY(norms(h, h->A[cur], ld, n, h->scal + 8));
+        SDC_TRY(norms(h, h->B[cur], ld, n, h->scal + 10));
+        SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + 8, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        SDC_CK(cudaStreamSynchronize(h->st));
+        const double fa = h->hscal[1], fb = h->hscal[3];
+        const double sd = fa + fb > 0.0 ? fb / (fa + fb) : 0.5;
+        if (sd < 1e-6 || sd > 1.0 - 1e-6) { p = j + 1; break; }
+      }
       if (stop_mode == SDC_STOP_RTEST && j >= 1) {
         SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + SCAL_HIST + j, sizeof(double), cudaMemcpyDeviceToHost, h->st));
         SDC_CK(cudaStreamSynchronize(h->st));
@@ -1333,6 +1481,11 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
         SDC_CK(cudaStreamSynchronize(h->st));
         if (j < hist_cap) { hbuf[3 * j] = h->hscal[0]; hbuf[3 * j + 1] = h->hscal[1]; }
         if (h->hscal[1] <= tol) { p = j + 1; conv = 1; break; }
+        // plateau: a metric within 10 tol that no longer halves -- the rounding floor
+        if ((flags & SDC_FLAG_PLATEAU) && h->hscal[1] <= 10.0 * tol && h->hscal[1] > 0.5 * prev) {
+          p = j + 1; conv = 1; break;
+        }
+        prev = h->hscal[1];
       }
     }
     SDC_TRY(enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, have_split, cur, max_iters));
@@ -1348,6 +1501,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   res->metric_fro = sc[6];
   res->iters = p;
   res->converged = conv;
+  res->side = sc[9] + sc[11] > 0.0 ? sc[11] / (sc[9] + sc[11]) : 0.5;
   res->status = (h->hflags[0] || !std::isfinite(res->metric)) ? SDC_STATUS_NONFINITE
                : (res->metric <= SDC_SPLIT_ACCEPT ? SDC_STATUS_SPLIT : SDC_STATUS_NO_SPLIT);
   return 0;
