@@ -21,7 +21,7 @@ _lib = None
 
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
 REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
-FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED = 1, 2, 4
+FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED, FLAG_QL_ORTH = 1, 2, 4, 8
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
 SPLIT_ACCEPT = 1e-8
 

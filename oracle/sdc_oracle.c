@@ -469,6 +469,19 @@ int orc_split(int n, const double *A, int lda, const double *B, int ldb,
                           hist_cap, res);
 }
 
+/* Cheaper left basis for pencils: the left deflating
+ * subspace of the |lambda| > 1 part is A X for X = span Q_R(:, 1:r) (A is nonsingular on it:
+ * A x = lambda B x with lambda != 0, infinite eigenvalues included), and QR preserves nested
+ * column spans, so Q_L := Q of QR(A Q_R) (diag R >= 0) spans it for every r at once. */
+static void ql_from_aq(int n, const double *A, int lda, const double *Q, int ldq, double *QL, int ldql) {
+  double *W = (double *)malloc(sizeof(double) * (size_t)n * n), *tau = (double *)malloc(sizeof(double) * n);
+  orc_gemm(0, 0, n, n, n, A, lda, Q, ldq, W, n);
+  orc_geqr2(n, n, W, n, tau);
+  orc_org2r_signed(n, W, n, tau, QL, ldql);
+  free(W);
+  free(tau);
+}
+
 int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
                      const double *V, int ldv, const double *VL, int ldvl,
                      int region, double param, int flags,
@@ -478,14 +491,16 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   if (region < 0 || region > 2) return -30;
   if (region == ORC_REGION_DISK && !(param > 0.0)) return -31;
   if ((region == ORC_REGION_HALFPLANE || (flags & ORC_FLAG_SYMMETRIC)) && B) return -32;
-  if (flags & ~(ORC_FLAG_SYMMETRIC | ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED)) return -33;
+  if (flags & ~(ORC_FLAG_SYMMETRIC | ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED | ORC_FLAG_QL_ORTH)) return -33;
+  if ((flags & ORC_FLAG_QL_ORTH) && !B) return -34;
+  const int ql_orth = (flags & ORC_FLAG_QL_ORTH) != 0;   /* no left IRS: Q_L from QR(A Q_R) */
   const int sym = (flags & ORC_FLAG_SYMMETRIC) != 0;
   const double rho = region == ORC_REGION_DISK ? param : 1.0;
   if (n < 2) return -1;
   if (lda < n) return -3;
   if (B && ldb < n) return -5;
   if (!V || ldv < n) return -6;
-  if (B && (!VL || ldvl < n)) return -8;
+  if (B && !(flags & ORC_FLAG_QL_ORTH) && (!VL || ldvl < n)) return -8;
   if (max_iters < 1) return -10;
   if (!(tol >= 0.0)) return -11;
   if (stop_mode < 0 || stop_mode > 2) return -12;
@@ -522,7 +537,7 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   int have_split = 0;
   for (int j = 0; j < max_iters; ++j) {
     orc_irs_pass(n, Aj, n, Bj, n, Aj, n, Bj, n, Rc);
-    if (pencil) orc_irs_pass(n, Lj, n, Mj, n, Lj, n, Mj, n, NULL);
+    if (pencil && !ql_orth) orc_irs_pass(n, Lj, n, Mj, n, Lj, n, Mj, n, NULL);
     if ((flags & ORC_FLAG_ONESIDED) && stop_mode == ORC_STOP_E21 && j >= 2) {
       /* every eigenvalue on one side: (A^{-1}B)^{2^p} -> 0 or infinity, one of A_p, B_p
        * vanishes relative to the other -- no split exists, stop */
@@ -543,7 +558,11 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
     if (stop_mode == ORC_STOP_E21) {
       orc_grurv_right(n, Aj, n, Bj, n, V, ldv, Q, ldq, NULL, NULL);
       const double *QLm = Q; int ldqlm = ldq;
-      if (pencil) { orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n); QLm = QLw; ldqlm = n; }
+      if (pencil) {
+        if (ql_orth) ql_from_aq(n, A, lda, Q, ldq, QLw, n);
+        else orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n);
+        QLm = QLw; ldqlm = n;
+      }
       met = similarity_and_select(n, A, lda, B, ldb, Q, ldq, QLm, ldqlm, nA, nB, fA, fB,
                                   Ah, Bh, &r, &mfro, sym);
       have_split = 1;
@@ -559,7 +578,11 @@ int orc_split_region(int n, const double *A, int lda, const double *B, int ldb,
   if (!have_split) {
     orc_grurv_right(n, Aj, n, Bj, n, V, ldv, Q, ldq, NULL, NULL);
     const double *QLm = Q; int ldqlm = ldq;
-    if (pencil) { orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n); QLm = QLw; ldqlm = n; }
+    if (pencil) {
+      if (ql_orth) ql_from_aq(n, A, lda, Q, ldq, QLw, n);
+      else orc_grurv_left(n, Lj, n, Mj, n, VL, ldvl, QLw, n);
+      QLm = QLw; ldqlm = n;
+    }
     met = similarity_and_select(n, A, lda, B, ldb, Q, ldq, QLm, ldqlm, nA, nB, fA, fB,
                                 Ah, Bh, &r, &mfro, sym);
   }

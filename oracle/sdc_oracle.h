@@ -14,8 +14,9 @@ enum { ORC_STOP_FIXED = 0, ORC_STOP_RTEST = 1, ORC_STOP_E21 = 2 };
 enum { ORC_REGION_UNIT_DISK = 0, ORC_REGION_DISK = 1, ORC_REGION_HALFPLANE = 2 };
 enum { ORC_FLAG_SYMMETRIC = 1,
        ORC_FLAG_PLATEAU = 2,   /* E21 mode: also stop at a metric <= 10 tol that stopped halving */
-       ORC_FLAG_ONESIDED = 4   /* E21 mode: stop after pass >= 3 once ||B_p||/(||A_p||+||B_p||) is
-                                  within 1e-6 of 0 or 1 (every eigenvalue on one side)       */ };
+       ORC_FLAG_ONESIDED = 4,  /* E21 mode: stop after pass >= 3 once ||B_p||/(||A_p||+||B_p||) is
+                                  within 1e-6 of 0 or 1 (every eigenvalue on one side)       */
+       ORC_FLAG_QL_ORTH = 8    /* pencils: no left IRS; Q_L = Q of QR(A Q_R), diag R >= 0    */ };
 enum { ORC_STATUS_SPLIT = 0, ORC_STATUS_NO_SPLIT = 1, ORC_STATUS_NONFINITE = 2 };
 #define ORC_SPLIT_ACCEPT 1e-8 /* split_accept_tol (SPEC.md design decision; Q4) */
 
