@@ -398,11 +398,12 @@ def main():
             return 0
         return run_trevc(args, rank, world, local)
     n = args.n or inputs.CONFIG_N[cfg]
-    pencil = cfg == 4
+    pencil = cfg in (4, 9)
+    ql_orth = cfg == 9
     cfg_name = f"cfg{cfg}: " + inputs.CONFIG_DOC[cfg] + ("" if args.n is None else f" [n overridden to {n}]")
 
     if args.impl == "reference":
-        passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30, 6: 30}[cfg]
+        passes = args.passes or {1: 12, 2: 20, 3: 30, 4: 30, 5: 30, 6: 30, 9: 30}[cfg]
         return run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg)
 
     import numpy as np
@@ -422,7 +423,9 @@ def main():
         p = inputs.Problem("cfg6", n, A6, None, V6, None, 30, 0.0, 0,
                            expected_k=2 * int(np.sum(s6 < 1)))
     else:
-        p = inputs.make_config(cfg, n=n, device=dev)
+        p = inputs.make_config(4 if ql_orth else cfg, n=n, device=dev)
+        if ql_orth:
+            p.VL = None
     passes = args.passes or p.max_iters
     stop = {0: "fixed", 1: "rtest", 2: "e21"}[p.stop]
     torch.cuda.synchronize()
@@ -435,7 +438,8 @@ def main():
         if svd:
             q, _, info = h.svd_split(p.A, 1.0, p.V, max_iters=passes, Q=Q)
             return q, None, None, info
-        return h.split(p.A, p.B, p.V, p.VL, max_iters=passes, tol=p.tol, stop=stop, Q=Q, QL=QL)
+        return h.split(p.A, p.B, p.V, p.VL, max_iters=passes, tol=p.tol, stop=stop, Q=Q, QL=QL,
+                       ql_orth=ql_orth)
 
     def barrier():
         if world > 1:
@@ -475,6 +479,8 @@ def main():
     ms = max_over_ranks(ms, world, dev)
     info = infos[-1]
     F = flop_model(n, info.iters, pencil, monitor=(stop == "e21"))
+    if ql_orth:   # the right IRS + GRURV + similarities, plus A Q_R and QR(A Q_R) with explicit Q
+        F = flop_model(n, info.iters) + (2.0 + 8.0 / 3.0 + 4.0) * n ** 3
     value = replica_throughput(ms, world)
     tflops = F / (ms / 1e3) / 1e12
 
@@ -502,6 +508,31 @@ def main():
         ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
         e2e = {"value": replica_throughput(ms_e2e, world), "unit": "split steps/s",
                "h2d_bytes_per_step": m6 * m6 * 8, "d2h_bytes_per_step": n * n * 8,
+               "ms_per_step": ms_e2e, "steps": args.e2e_steps}
+    elif args.e2e_steps > 0 and ql_orth:
+        # public Python API with pinned host buffers: A, B, V -> device, split, Q, Q_L -> host
+        hs = [torch.empty((n, n), dtype=torch.float64, pin_memory=True) for _ in range(5)]
+        for hx, x in zip(hs[:3], (p.A, p.B, p.V)):
+            hx.copy_(x.t())
+        ds = [torch.empty((n, n), dtype=torch.float64, device=dev) for _ in range(3)]
+
+        def e2e_step():
+            for d, hx in zip(ds, hs[:3]):
+                d.copy_(hx, non_blocking=True)
+            q, ql, _, _ = h.split(ds[0].t(), ds[1].t(), ds[2].t(), None, max_iters=passes, Q=Q, QL=QL,
+                                  ql_orth=True)
+            hs[3].copy_(q.t(), non_blocking=True)
+            hs[4].copy_(ql.t(), non_blocking=True)
+        e2e_step()
+        barrier()
+        e0.record(st)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(st)
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, world, dev)
+        e2e = {"value": replica_throughput(ms_e2e, world), "unit": "split steps/s",
+               "h2d_bytes_per_step": 3 * n * n * 8, "d2h_bytes_per_step": 2 * n * n * 8,
                "ms_per_step": ms_e2e, "steps": args.e2e_steps}
     elif args.e2e_steps > 0:
         def pinned(x):

@@ -64,8 +64,12 @@ enum { SDC_FLAG_SYMMETRIC = 1, /* RSEP, Alg. 6: Ahat <- (Ahat
                                   before the split selection; B = I only                     */
        SDC_FLAG_PLATEAU = 2,   /* SDC_STOP_E21 only: also stop once the metric is <= 10 tol and
                                   no longer halves (the rounding floor)       */
-       SDC_FLAG_ONESIDED = 4   /* SDC_STOP_E21 only: stop after pass >= 3 once res.side is within
-                                  1e-6 of 0 or 1 (no eigenvalue on one side of the boundary) */ };
+       SDC_FLAG_ONESIDED = 4,  /* SDC_STOP_E21 only: stop after pass >= 3 once res.side is within
+                                  1e-6 of 0 or 1 (no eigenvalue on one side of the boundary) */
+       SDC_FLAG_QL_ORTH = 8    /* pencils: no left IRS / left GRURV; Q_L = Q of
+                                  QR(A Q_R), diag R >= 0 (same left deflating subspace as Alg. 4,
+                                  Q_L^T A Q_R upper triangular, the split chosen by F21); VL may
+                                  be NULL.  Halves the pencil step            */ };
 enum { SDC_STATUS_SPLIT = 0, SDC_STATUS_NO_SPLIT = 1, SDC_STATUS_NONFINITE = 2 };
 #define SDC_SPLIT_ACCEPT 1e-8 /* status 0 iff metric <= this (reading Q4)       */
 

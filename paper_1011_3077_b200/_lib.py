@@ -10,7 +10,7 @@ LIB_PATH = os.path.join(HERE, "libsdc.so")
 STOP_FIXED, STOP_RTEST, STOP_E21 = 0, 1, 2
 STATUS_SPLIT, STATUS_NO_SPLIT, STATUS_NONFINITE = 0, 1, 2
 REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
-FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED = 1, 2, 4
+FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED, FLAG_QL_ORTH = 1, 2, 4, 8
 PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PROF_GEMM_OTHER = 0, 1, 2, 3, 4, 5, 6
 SPLIT_ACCEPT = 1e-8
 

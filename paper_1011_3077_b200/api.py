@@ -99,7 +99,7 @@ class Handle:
     # ---- the step ---------------------------------------------------------------------
     def split(self, A, B=None, V=None, VL=None, max_iters=12, tol=0.0, stop="fixed",
               Q=None, QL=None, want_ahat=False, hist_cap=None, region="unit_disk", param=1.0,
-              symmetric=False):
+              symmetric=False, ql_orth=False):
         """sdc_split_region: returns (Q, QL or None, Ahat or None, SplitInfo).
         region: "unit_disk" | "disk" (|z| < param) | "halfplane" (Re z < param)."""
         n = A.shape[0]
@@ -124,7 +124,9 @@ class Handle:
         reg = {"unit_disk": _lib.REGION_UNIT_DISK, "disk": _lib.REGION_DISK,
                "halfplane": _lib.REGION_HALFPLANE}[region]
         rc = self.lib.sdc_split_region(self._h, _stream(dev), n, pa, la, pb, lb, pv, lv, pvl, lvl,
-                                       reg, float(param), _lib.FLAG_SYMMETRIC if symmetric else 0,
+                                       reg, float(param),
+                                       (_lib.FLAG_SYMMETRIC if symmetric else 0) |
+                                       (_lib.FLAG_QL_ORTH if ql_orth else 0),
                                        max_iters, float(tol), STOPS[stop], pq, lq, pql, lql, pah,
                                        lah, hist.ctypes.data_as(ctypes.c_void_p), hist_cap,
                                        ctypes.byref(res))

@@ -90,6 +90,7 @@ struct sdc_handle {
   bool cluster_ok = false;             // 16-CTA clusters usable for the panel kernel
   bool mcluster_ok = false;            // several co-resident 16-CTA clusters (tall panels)
   bool panel_reg = true;               // register-resident panel column loop (rows_per <= 256)
+  bool ql_orth = false;                // current call: SDC_FLAG_QL_ORTH
   int max_clusters16 = 0;
   int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width (multiple of 64)
@@ -805,6 +806,22 @@ int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const d
   return 0;
 }
 
+// Cheaper pencil left basis (SDC_FLAG_QL_ORTH): Q_L = Q of QR(A Q_R) with
+// diag R >= 0 -- A X spans the left deflating subspace of the outside eigenvalues for every
+// leading column block X of Q_R, and QR preserves nested column spans.
+int ql_from_aq(sdc_handle* h, int n, const double* A, long long lda, const double* Q, long long ldq,
+               double* QL, long long ldql) {
+  const long long ld = n;
+  const Fac f = fac_square(h, n);
+  SDC_TRY(transpose_rev(h, h->G3, ld, A, lda, n, 0));                   // A^T (K-major)
+  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->G3, ld, Q, ldq, 0.0, h->G2, ld));  // W = A Q_R
+  SDC_TRY(blocked_qr(h, h->G2, ld, n, n, f));
+  SDC_TRY(form_q(h, n, f, QL, ldql));
+  k_col_sign<<<ew_grid((long long)n * n), 256, 0, h->st>>>(QL, ldql, n, n, h->G2, ld);
+  SDC_LAUNCHED(h);
+  return 0;
+}
+
 int select_dev(sdc_handle* h, int n, const double* Ah, long long ldah, const double* Bh,
                long long ldbh, const double* nrmA, const double* nrmB, double* sel) {
   const int nblk = cdiv(n, SEL_T);
@@ -918,7 +935,7 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
   SDC_LAUNCHED(h);
   k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
   SDC_LAUNCHED(h);
-  if (pencil) {   // left IRS on (A^T, B^T)
+  if (pencil && !h->ql_orth) {   // left IRS on (A^T, B^T)
     SDC_TRY(transpose_rev(h, h->AL[0], ld, A, lda, n, 0));
     SDC_TRY(transpose_rev(h, h->BL[0], ld, B, ldb, n, 0));
     if (rho != 1.0) {
@@ -929,7 +946,7 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
     SDC_LAUNCHED(h);
   }
   SDC_TRY(transpose_rev(h, h->Vt, ld, V, ldv, n, 0));                   // V^T (K-major operand)
-  if (pencil) SDC_TRY(transpose_rev(h, h->VLt, ld, VL, ldvl, n, 0));
+  if (pencil && !h->ql_orth) SDC_TRY(transpose_rev(h, h->VLt, ld, VL, ldvl, n, 0));
   return 0;
 }
 
@@ -940,7 +957,8 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
   const bool pencil = B != nullptr;
   if (!have_split) {
     SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
-    if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+    if (pencil && h->ql_orth) SDC_TRY(ql_from_aq(h, n, A, lda, Q, ldq, QLd, ld));
+    else if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
     SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
   }
   SDC_TRY(norms(h, h->A[cur], ld, n, h->scal + 8));    // side indicator (res->side)
@@ -970,7 +988,7 @@ int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const do
   for (int j = 0; j < max_iters; ++j) {
     SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S, j,
                      nullptr, 0));
-    if (pencil)
+    if (pencil && !h->ql_orth)
       SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
                        h->SL, -1, nullptr, 0));
     cur ^= 1;
@@ -1377,7 +1395,12 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     set_err("half-plane regions and the symmetric flag take B = NULL (B = I)");
     return -6;
   }
-  if (flags & ~(SDC_FLAG_SYMMETRIC | SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED)) { set_err("unknown flags"); return -14; }
+  if (flags & ~(SDC_FLAG_SYMMETRIC | SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED | SDC_FLAG_QL_ORTH)) {
+    set_err("unknown flags");
+    return -14;
+  }
+  if ((flags & SDC_FLAG_QL_ORTH) && !B) { set_err("SDC_FLAG_QL_ORTH needs a pencil (B != NULL)"); return -6; }
+  h->ql_orth = (flags & SDC_FLAG_QL_ORTH) != 0;
   h->region = region;
   h->rparam = region == SDC_REGION_UNIT_DISK ? 1.0 : region_param;
   h->rflags = flags;
@@ -1389,8 +1412,8 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   if (pencil && !h->pencil) { set_err("handle created without pencil workspace"); return -6; }
   if (!V) { set_err("V is NULL"); return -8; }
   if (ldv < n) { set_err("ldv < n"); return -9; }
-  if (pencil && !VL) { set_err("VL is NULL for a pencil"); return -10; }
-  if (pencil && ldvl < n) { set_err("ldvl < n"); return -11; }
+  if (pencil && !h->ql_orth && !VL) { set_err("VL is NULL for a pencil"); return -10; }
+  if (pencil && !h->ql_orth && ldvl < n) { set_err("ldvl < n"); return -11; }
   if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -13; }
   if (!(tol >= 0.0)) { set_err("tol < 0"); return -14; }
   if (stop_mode < 0 || stop_mode > 2) { set_err("unknown stop mode"); return -15; }
@@ -1453,7 +1476,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     for (int j = 0; j < max_iters; ++j) {
       SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S,
                        j, nullptr, 0));
-      if (pencil)
+      if (pencil && !h->ql_orth)
         SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
                          h->SL, -1, nullptr, 0));
       cur ^= 1;
@@ -1474,7 +1497,8 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
       }
       if (stop_mode == SDC_STOP_E21) {
         SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
-        if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+        if (pencil && h->ql_orth) SDC_TRY(ql_from_aq(h, n, A, lda, Q, ldq, QLd, ld));
+        else if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
         SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
         have_split = true;
         SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));

@@ -150,7 +150,9 @@ CONFIG_DOC = {
     6: "singular-value split (f3, PAPER.md:453): A 8192x8192 = U diag(s) W^T (seed 8), s in [.05,.8] (half) "
        "and [1.25,20], rho=1, RSEP step on the order-16384 embedding [[0,A],[A^T,0]], V seed 1008, 30 passes",
 }
-CONFIG_N = {1: 64, 2: 1024, 3: 4096, 4: 8192, 5: 16384, 6: 16384}
+CONFIG_DOC[9] = ("config 4's pencil (n=8192, seeds 4,5, V_R seed 1004), 30 passes, with the cheaper left "
+                 "basis Q_L = Q of QR(A Q_R) (SDC_FLAG_QL_ORTH, f3): no left IRS")
+CONFIG_N = {1: 64, 2: 1024, 3: 4096, 4: 8192, 5: 16384, 6: 16384, 9: 8192}
 
 
 def make_config(cfg: int, n: int | None = None, device=None) -> Problem:
