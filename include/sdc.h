@@ -153,6 +153,23 @@ int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, in
                   const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
                   int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res);
 
+/* Batched small-n split step: `batch` independent RNEP steps on the
+ * unit disk (Alg. 5, FIXED passes), one CTA per problem with the whole step in shared
+ * memory (unblocked routines in the oracle's order: dgeqr2, complement, GRURV via dgerq2 /
+ * dorgr2, similarity with the original A, split selection).  2 <= n <= 64.
+ *  1 h, 2 stream
+ *  3 batch      >= 0 problems
+ *  4 n          order of every problem
+ *  5 A, 6 lda, 7 strideA   problem b at A + b strideA (device), ld lda >= n, stride >= lda n
+ *  8 V, 9 ldv, 10 strideV  Haar V of problem b (device)
+ * 11 max_iters  IRS passes (>= 1)
+ * 12 Q, 13 ldq, 14 strideQ out (device): Q of problem b
+ * 15 res        HOST out: batch sdc_result (iters = max_iters, converged = 0, side = NaN)
+ * Synchronises `stream`. */
+int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const double* A, int lda,
+                      long long strideA, const double* V, int ldv, long long strideV, int max_iters,
+                      double* Q, int ldq, long long strideQ, sdc_result* res);
+
 /* Recursive divide-and-conquer to block upper triangular form A = Q T Q^T (
  * PAPER.md:406-410 "zero E21 and recurse on (A11, A22)", random splitting lines
  * PAPER.md:472-475 restricted to real arithmetic: vertical lines Re z = a).

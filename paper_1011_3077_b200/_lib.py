@@ -32,6 +32,7 @@ _SIGS = {
     "sdc_split_region": (I, [P, P, I, P, I, P, I, P, I, P, I, I, D, I, I, D, I, P, I, P, I, P, I, P, I,
                              ctypes.POINTER(SdcResult)]),
     "sdc_trevc": (I, [P, P, I, P, I, P, I, P, I]),
+    "sdc_split_batched": (I, [P, P, I, I, P, I, LL, P, I, LL, I, P, I, LL, P]),
     "sdc_schur": (I, [P, P, I, P, I, I, ctypes.c_ulonglong, I, D, P, I, P, I, P, P,
                       ctypes.POINTER(I), P, ctypes.POINTER(D)]),
     "sdc_svd_split": (I, [P, P, I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,

@@ -159,6 +159,25 @@ class Handle:
         return Q, Ah, SplitInfo(res.k, res.r, res.metric, res.metric_fro, res.iters, res.converged,
                                 res.status, hist)
 
+    def split_batched(self, A, V, max_iters=12, Q=None):
+        """sdc_split_batched: A, V of shape (batch, n, n) with each A[b] column-major (e.g.
+        A = X.transpose(1, 2).contiguous().transpose(1, 2)); returns (Q, [SplitInfo])."""
+        batch, n, _ = A.shape
+        for x in (A, V):
+            if x.dtype != torch.float64 or not x.is_cuda or x.stride(1) != 1 or x.stride(2) < n:
+                raise ValueError("expected (batch, n, n) column-major float64 CUDA tensors")
+        if Q is None:
+            Q = torch.empty((batch, n, n), dtype=torch.float64, device=A.device).transpose(1, 2)
+        res = (SdcResult * max(1, batch))()
+        check(self.lib.sdc_split_batched(self._h, _stream(A.device), batch, n,
+                                         ctypes.c_void_p(A.data_ptr()), A.stride(2), A.stride(0),
+                                         ctypes.c_void_p(V.data_ptr()), V.stride(2), V.stride(0),
+                                         max_iters, ctypes.c_void_p(Q.data_ptr()), Q.stride(2),
+                                         Q.stride(0), res), "sdc_split_batched")
+        infos = [SplitInfo(r.k, r.r, r.metric, r.metric_fro, r.iters, r.converged, r.status, None)
+                 for r in res[:batch]]
+        return Q, infos
+
     def schur(self, A, leaf=1, seed=1, max_iters=60, tol=1e-13, Q=None, T=None):
         """sdc_schur: recursive divide-and-conquer A = Q T Q^T.
         Returns (Q, T, blocks [(offset, size)], stats dict)."""

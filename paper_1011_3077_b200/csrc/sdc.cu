@@ -29,6 +29,7 @@
 #include "gemm_tma.cuh"
 #include "panel.cuh"
 #include "trevc.cuh"
+#include "batched.cuh"
 
 using namespace sdc;
 
@@ -75,6 +76,8 @@ struct sdc_handle {
   double *G1 = nullptr, *G2 = nullptr, *G3 = nullptr, *T1 = nullptr, *Ah = nullptr, *Bh = nullptr;
   double *QLb = nullptr, *Rprev = nullptr;
   double* Emb = nullptr;               // hermitian embedding of sdc_svd_split (lazy, n_max^2)
+  double* bat_out = nullptr;           // sdc_split_batched per-problem results (lazy)
+  size_t bat_out_n = 0;
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
   double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
   unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
@@ -1039,6 +1042,7 @@ void sdc_destroy(sdc_handle* h) {
   if (h->hscal) cudaFreeHost(h->hscal);
   if (h->hflags) cudaFreeHost(h->hflags);
   for (void* p : h->allocs) cudaFree(p);
+  if (h->bat_out) cudaFree(h->bat_out);
   delete h;
 }
 
@@ -1305,6 +1309,63 @@ int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int 
   rc = run();
   cleanup();
   return rc;
+}
+
+int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const double* A, int lda,
+                      long long strideA, const double* V, int ldv, long long strideV, int max_iters,
+                      double* Q, int ldq, long long strideQ, sdc_result* res) {
+  SDC_TRY(check_handle(h));
+  if (batch < 0) { set_err("batch < 0"); return -3; }
+  if (n < 2 || n > BAT_NMAX) { set_err("batched n=%d outside [2, %d]", n, BAT_NMAX); return -4; }
+  if (!A && batch) { set_err("A is NULL"); return -5; }
+  if (lda < n) { set_err("lda < n"); return -6; }
+  if (strideA < (long long)lda * n) { set_err("strideA < lda n"); return -7; }
+  if (!V && batch) { set_err("V is NULL"); return -8; }
+  if (ldv < n) { set_err("ldv < n"); return -9; }
+  if (strideV < (long long)ldv * n) { set_err("strideV < ldv n"); return -10; }
+  if (max_iters < 1) { set_err("max_iters < 1"); return -11; }
+  if (!Q && batch) { set_err("Q is NULL"); return -12; }
+  if (ldq < n) { set_err("ldq < n"); return -13; }
+  if (strideQ < (long long)ldq * n) { set_err("strideQ < ldq n"); return -14; }
+  if (!res && batch) { set_err("res is NULL"); return -15; }
+  if (batch == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->st = st;
+  const size_t smem = bat_smem_doubles() * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    SDC_CK(cudaFuncSetAttribute(k_split_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  if ((size_t)batch * 4 > h->bat_out_n) {
+    if (h->bat_out) cudaFree(h->bat_out);
+    h->bat_out = nullptr;
+    h->bat_out_n = 0;
+    if (cudaMalloc(&h->bat_out, (size_t)batch * 4 * sizeof(double)) != cudaSuccess) {
+      set_err("sdc_split_batched: out of memory");
+      return SDC_ERR_NOMEM;
+    }
+    h->bat_out_n = (size_t)batch * 4;
+  }
+  BatArgs a{A, lda, strideA, V, ldv, strideV, Q, ldq, strideQ, h->bat_out, n, max_iters};
+  k_split_batched<<<batch, BAT_THREADS, smem, st>>>(a);
+  SDC_LAUNCHED(h);
+  std::vector<double> out((size_t)batch * 4);
+  SDC_CK(cudaMemcpyAsync(out.data(), h->bat_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SDC_CK(cudaStreamSynchronize(st));
+  for (int b = 0; b < batch; ++b) {
+    sdc_result& r = res[b];
+    r.r = (int)out[4 * b];
+    r.k = n - r.r;
+    r.metric = out[4 * b + 1];
+    r.metric_fro = out[4 * b + 2];
+    r.iters = max_iters;
+    r.converged = 0;
+    r.side = NAN;
+    r.status = (out[4 * b + 3] != 0.0 || !std::isfinite(r.metric)) ? SDC_STATUS_NONFINITE
+               : (r.metric <= SDC_SPLIT_ACCEPT ? SDC_STATUS_SPLIT : SDC_STATUS_NO_SPLIT);
+  }
+  return 0;
 }
 
 int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, const double* Q,
