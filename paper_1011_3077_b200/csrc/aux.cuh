@@ -432,31 +432,59 @@ __global__ void k_nonfinite(const double* X, long long ldx, int n, int* flag) {
 
 // WY reduction for split-K partials:  W(:, c) = op(T) * sum_s Wp[s](:, c)
 //   trans = 1: W = T^T W0 (apply H^T = I - Y T^T Y^T, i.e. Q^T C);  trans = 0: W = T W0.
-// One CTA (256 threads) per block of WYR_COLS columns; T staged in smem.
+// One CTA (256 threads) per block of cpb <= WYR_COLS columns (cpb chosen by the host so the
+// grid covers the SMs even for the 64..192-column inner updates); when a block has fewer
+// than 256 entries, g = 256 / (cpb nb) thread groups sum interleaved split slices and the
+// group sums are added in a fixed order (deterministic).  T staged in smem.
 constexpr int WYR_COLS = 16;
 __global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits, long long zstride,
                                                    int nb, int ncols, const double* T, int trans,
-                                                   double* W) {
+                                                   double* W, int cpb) {
   __shared__ double Ts[64 * 64];
-  __shared__ double w0[WYR_COLS][64];
+  __shared__ double part[WYR_COLS * 64];
+  __shared__ double w0[WYR_COLS * 64];
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) Ts[e] = T[e];
-  const int c0 = blockIdx.x * WYR_COLS;
-  for (int e = threadIdx.x; e < WYR_COLS * nb; e += blockDim.x) {
-    int cc = e / nb, i = e % nb, c = c0 + cc;
-    double s = 0.0;
-    if (c < ncols)
-      for (int z = 0; z < splits; ++z) s += Wp[(long long)z * zstride + i + (long long)c * nb];
-    w0[cc][i] = s;
+  const int c0 = blockIdx.x * cpb;
+  const int elems = cpb * nb;
+  const int g = elems >= (int)blockDim.x ? 1 : (int)blockDim.x / elems;
+  if (g == 1) {
+    for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+      const int c = c0 + e / nb;
+      double s = 0.0;
+      if (c < ncols) {
+        const double* p = Wp + (e % nb) + (long long)c * nb;
+        for (int z = 0; z < splits; ++z) s += p[(long long)z * zstride];
+      }
+      w0[e] = s;
+    }
+  } else {
+    const int e = threadIdx.x % elems, q = threadIdx.x / elems;
+    if (q < g) {
+      const int c = c0 + e / nb;
+      double s = 0.0;
+      if (c < ncols) {
+        const double* p = Wp + (e % nb) + (long long)c * nb;
+        for (int z = q; z < splits; z += g) s += p[(long long)z * zstride];
+      }
+      part[q * elems + e] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < elems) {
+      double s = part[threadIdx.x];
+      for (int r = 1; r < g; ++r) s += part[r * elems + threadIdx.x];
+      w0[threadIdx.x] = s;
+    }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < WYR_COLS * nb; e += blockDim.x) {
-    int cc = e / nb, i = e % nb, c = c0 + cc;
+  for (int e = threadIdx.x; e < elems; e += blockDim.x) {
+    const int cc = e / nb, i = e % nb, c = c0 + cc;
     if (c >= ncols) continue;
+    const double* w = w0 + cc * nb;
     double s = 0.0;
     if (trans) {   // (T^T w)(i) = sum_{l <= i} T(l, i) w(l)
-      for (int l = 0; l <= i; ++l) s = fma(Ts[i * nb + l], w0[cc][l], s);
+      for (int l = 0; l <= i; ++l) s = fma(Ts[i * nb + l], w[l], s);
     } else {       // (T w)(i) = sum_{l >= i} T(i, l) w(l)
-      for (int l = i; l < nb; ++l) s = fma(Ts[l * nb + i], w0[cc][l], s);
+      for (int l = i; l < nb; ++l) s = fma(Ts[l * nb + i], w[l], s);
     }
     W[i + (long long)c * nb] = s;
   }

@@ -98,6 +98,13 @@ struct sdc_handle {
   int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width (multiple of 64)
   double *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr, *Gb = nullptr;
+  // look-ahead QR (blocked_qr): panels and the next block's update on a high-priority
+  // handle stream, the bulk trailing update of each outer block on the caller's stream with
+  // its own split-K workspace (Wp2, W2, Zb2)
+  bool lookahead = true;
+  cudaStream_t st_hi = nullptr;
+  cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
+  double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
   // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
   struct GraphKey {
     int n = 0, max_iters = 0, nbo = 0, region = 0, rflags = 0;
@@ -196,8 +203,8 @@ struct ProfScope {
 };
 void prof_collect(sdc_handle* h) {
   if (h->recs.empty()) return;
-  cudaEventSynchronize(h->ev_pool[h->recs.back().e1]);
-  for (auto& r : h->recs) {
+  for (auto& r : h->recs) {   // events may sit on two streams (look-ahead QR): wait for each
+    cudaEventSynchronize(h->ev_pool[r.e1]);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev_pool[r.e0], h->ev_pool[r.e1]);
     h->prof_ms[r.cls] += ms;
@@ -483,8 +490,9 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
   SDC_TRY(rc0);
   {
     ProfScope ps(h, SDC_PROF_WYRED, 8.0 * ((double)splits * nb * ncols + (double)nb * ncols));
-    k_wy_reduce<<<cdiv(ncols, WYR_COLS), 256, 0, h->st>>>(h->Wp, splits, (long long)nb * ncols, nb,
-                                                          ncols, T, trans, h->W);
+    const int cpb = std::max(1, std::min(WYR_COLS, ncols / (2 * h->num_sms)));
+    k_wy_reduce<<<cdiv(ncols, cpb), 256, 0, h->st>>>(h->Wp, splits, (long long)nb * ncols, nb, ncols,
+                                                     T, trans, h->W, cpb);
     SDC_LAUNCHED(h);
   }
   h->gemm_sub = SDC_PROF_GEMM_UPD;
@@ -653,10 +661,78 @@ int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, 
   return rc1;
 }
 
+// panels + inner WY updates + T_O of the outer block at I0 (columns I0..I0+nbo-1 only)
+int factor_block(sdc_handle* h, double* A, long long lda, int m, int n, int I0, int nbo, const Fac& f) {
+  for (int i0 = I0; i0 < I0 + nbo; i0 += NB) {
+    const int nbp = std::min(NB, I0 + nbo - i0);
+    SDC_TRY(panel(h, A + i0 + (long long)i0 * lda, lda, m - i0, nbp, f.Y + i0 + (long long)i0 * f.ldy,
+                  f.ldy, f.Yt + i0 + (long long)i0 * f.ldyt, f.ldyt, Tblk(h, i0), h->tau + i0, i0 - I0));
+    const int rest = I0 + nbo - (i0 + nbp);
+    if (rest > 0)
+      SDC_TRY(wy_apply(h, 1, m - i0, rest, f.Yp(i0), f.ldy, f.Ytp(i0), f.ldyt, Tblk(h, i0), nbp,
+                       A + i0 + (long long)(i0 + nbp) * lda, lda));
+  }
+  return build_tout(h, m, I0, nbo, f);
+}
+
+// Look-ahead (depth 1) schedule of the two-level QR.  The critical chain -- panels, inner
+// updates, T_O, and the trailing update of the NEXT outer block's nbo columns -- runs on
+// the high-priority handle stream st_hi; the bulk trailing update of the remaining columns
+// runs on the caller's stream (own workspace) and overlaps the next block's panels, which
+// occupy only the panel kernel's clusters.  Same arithmetic as the serial order, per column
+// block; the split-K slicing of the bulk update differs (rounding-level only).
+struct LaScope {   // restores the caller's stream and the primary workspace on every exit
+  sdc_handle* h; cudaStream_t side;
+  explicit LaScope(sdc_handle* h_) : h(h_), side(h_->st) {}
+  void use_side(bool on) {
+    h->st = on ? side : h->st_hi;
+    if ((h->Wp2 != nullptr) && on != swapped) {
+      std::swap(h->Wp, h->Wp2); std::swap(h->W, h->W2); std::swap(h->Zb, h->Zb2);
+      swapped = on;
+    }
+  }
+  bool swapped = false;
+  ~LaScope() {
+    if (swapped) { std::swap(h->Wp, h->Wp2); std::swap(h->W, h->W2); std::swap(h->Zb, h->Zb2); }
+    h->st = side;
+  }
+};
+
+int blocked_qr_lookahead(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
+  LaScope la(h);
+  SDC_CK(cudaEventRecord(h->la_fork, la.side));
+  SDC_CK(cudaStreamWaitEvent(h->st_hi, h->la_fork, 0));
+  la.use_side(false);
+  bool pendingB = false;
+  for (int I0 = 0; I0 < n; I0 += h->nbo) {
+    const int nbo = std::min(h->nbo, n - I0);
+    SDC_TRY(factor_block(h, A, lda, m, n, I0, nbo, f));
+    const int c1 = I0 + nbo, rem = n - c1;
+    if (rem <= 0) break;
+    const int na = std::min(h->nbo, rem);
+    if (rem > na) SDC_CK(cudaEventRecord(h->la_fac, h->st_hi));
+    if (pendingB) SDC_CK(cudaStreamWaitEvent(h->st_hi, h->la_B, 0));
+    SDC_TRY(wy_apply_outer(h, 1, I0, nbo, m - I0, na, f, A + I0 + (long long)c1 * lda, lda));
+    if (rem > na) {
+      la.use_side(true);
+      SDC_CK(cudaStreamWaitEvent(la.side, h->la_fac, 0));
+      SDC_TRY(wy_apply_outer(h, 1, I0, nbo, m - I0, rem - na, f, A + I0 + (long long)(c1 + na) * lda, lda));
+      SDC_CK(cudaEventRecord(h->la_B, la.side));
+      la.use_side(false);
+      pendingB = true;
+    }
+  }
+  SDC_CK(cudaEventRecord(h->la_join, h->st_hi));
+  SDC_CK(cudaStreamWaitEvent(la.side, h->la_join, 0));
+  return 0;
+}
+
 // A (m x n, m >= n) <- Householder QR in place, two-level: 64-wide cooperative panels inside
 // nbo-wide outer blocks (inner WY updates restricted to the block), then one rank-nbo
 // trailing update per outer block.  Factors into f, T blocks into h->Tb / h->Tob.
 int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
+  if (h->lookahead && h->st_hi && h->nbo > NB && n > 2 * h->nbo)
+    return blocked_qr_lookahead(h, A, lda, m, n, f);
   for (int I0 = 0; I0 < n; I0 += h->nbo) {
     const int nbo = std::min(h->nbo, n - I0);
     for (int i0 = I0; i0 < I0 + nbo; i0 += NB) {
@@ -1039,6 +1115,9 @@ void sdc_destroy(sdc_handle* h) {
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
+  if (h->st_hi) cudaStreamDestroy(h->st_hi);
+  for (cudaEvent_t e : {h->la_fork, h->la_fac, h->la_B, h->la_join})
+    if (e) cudaEventDestroy(e);
   if (h->hscal) cudaFreeHost(h->hscal);
   if (h->hflags) cudaFreeHost(h->hflags);
   for (void* p : h->allocs) cudaFree(p);
@@ -1163,6 +1242,17 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaMallocHost(&h->hscal, sizeof(double) * (SCAL_HIST + MAX_HIST)) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
+  if (const char* e = getenv("SDC_LOOKAHEAD")) h->lookahead = atoi(e) != 0;
+  if (!rc && h->lookahead) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&h->st_hi, cudaStreamNonBlocking, greatest) != cudaSuccess) rc = SDC_ERR_CUDA;
+    for (cudaEvent_t* e : {&h->la_fork, &h->la_fac, &h->la_B, &h->la_join})
+      if (!rc && cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) rc = SDC_ERR_CUDA;
+    if (!rc) rc = dalloc(h, &h->Wp2, h->wp_elems);
+    if (!rc) rc = dalloc(h, &h->W2, (size_t)std::max(256, h->nbo) * (n + 64));
+    if (!rc) rc = dalloc(h, &h->Zb2, (size_t)h->nbo * (n + 64));
+  }
   if (rc) { sdc_destroy(h); return rc; }
   *out = h;
   return 0;

@@ -288,6 +288,40 @@ def test_outer_block_widths_parity(orc, sdc, nbo):
     assert info.k == p.expected_k
 
 
+@pytest.mark.parametrize("la", [0, 1])
+def test_lookahead_schedule_parity(orc, sdc, la):
+    # look-ahead QR (panels on a high-priority stream, bulk trailing updates overlapped on
+    # the caller's stream) and the serial order give the oracle's invariants at a ragged n
+    # with 4 outer blocks; the R of a 2n x n QR stays the unique diag >= 0 factor
+    h = _handle_with_env(sdc, 900, SDC_LOOKAHEAD=la)
+    p = inputs.make_config(2, n=900)
+    Q, _, Ah, info, o = run_both(orc, h, p)
+    assert_parity(o, Q, info, p.A, p.n, Ah)
+    assert info.k == p.expected_k
+    s = np.random.default_rng(78).standard_normal((1800, 900))
+    q, r = h.qr(dev(s))
+    _, r_o = orc.qr_signed(s)
+    assert np.allclose(host(r), r_o, rtol=0, atol=1e-12 * np.abs(r_o).max() * np.sqrt(900))
+    assert orth_err(host(q)) <= 64 * 900 * EPS
+
+
+def test_lookahead_graph_replay_matches_direct(sdc):
+    # the two-stream look-ahead schedule captured into the step's CUDA graph (fork/join by
+    # events) replays bit-identically to the directly launched sequence
+    p = inputs.make_config(2, n=800)
+    hg = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=4096, SDC_LOOKAHEAD=1)
+    hd = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=0, SDC_LOOKAHEAD=1)
+    A, V = dev(p.A), dev(p.V)
+    Qg = sdc.empty_colmajor(800, 800, A.device)
+    Qd = sdc.empty_colmajor(800, 800, A.device)
+    _, _, _, ig1 = hg.split(A, None, V, max_iters=6, Q=Qg)
+    q1 = Qg.clone()
+    _, _, _, ig2 = hg.split(A, None, V, max_iters=6, Q=Qg)
+    _, _, _, idd = hd.split(A, None, V, max_iters=6, Q=Qd)
+    assert torch.equal(q1, Qg) and torch.equal(Qg, Qd)
+    assert ig1.metric == ig2.metric == idd.metric and ig1.r == idd.r
+
+
 def test_blocked_qr_two_level_r_unique(orc, sdc):
     # R of the two-level QR equals the oracle's (unique with diag >= 0) at 2n x n, n = 700
     h = _handle_with_env(sdc, 700, SDC_NBO=256)
