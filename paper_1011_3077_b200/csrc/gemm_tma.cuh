@@ -92,6 +92,20 @@ SDC_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint6
       : "memory");
 }
 
+// Tensor-map acquire: the TMA unit caches descriptors by address, and the parameter buffer
+// of a launch may reuse an address a descriptor of an earlier (possibly concurrent) launch
+// occupied; acquiring through the tensormap proxy makes this launch's descriptor the one used.
+SDC_DEV void tmap_acquire(const CUtensorMap* tm) {
+#ifdef SDC_TMAP_FENCE
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(reinterpret_cast<uint64_t>(tm))
+               : "memory");
+#else
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
+#endif
+}
+
+SDC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 SDC_DEV int frag_row(int r) { return 2 * (r & 3) + (r >> 2); }   // conflict-free row map
 SDC_DEV int swz(int row, int k) { return row * 16 + ((((k >> 1) ^ (row & 7)) << 1) | (k & 1)); }
 
@@ -108,6 +122,7 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   uint64_t* empty = full + T::STAGES;
   uint64_t* cbar = empty + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { tmap_acquire(&tmA); tmap_acquire(&tmB); if (T::CPRE) tmap_acquire(&tmC); }
   // grouped rasterisation (no split-K): consecutive CTAs sweep GROUP M-tiles x all N-tiles
   // column by column, so the ~148 co-resident CTAs share A and B tiles in L2
   int bx = blockIdx.x, by = blockIdx.y;
@@ -163,6 +178,7 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   const bool producer = (threadIdx.x == 0);
   if (producer)
     for (int kt = 0; kt < min(ktiles, T::STAGES - 1); ++kt) issue(kt);
+  __syncwarp();
 
   // ---- consumers ----
   const int wm = warp % T::WARPS_M, wn = warp / T::WARPS_M;
@@ -187,6 +203,8 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % T::STAGES;
     if (producer && kt + T::STAGES - 1 < ktiles) issue(kt + T::STAGES - 1);
+    __syncwarp();   // the issuing lane may have waited on an "empty" barrier: reconverge warp 0
+                    // before the warp-wide mma.sync.aligned below
     mbar_wait(full + s, (kt / T::STAGES) & 1);
     const double* sA = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES);
     const double* sB = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES + T::A_BYTES);
@@ -206,6 +224,11 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
 #pragma unroll
         for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
+    // WAR across proxies: this warp's LDS reads of the slot (generic proxy) must be ordered
+    // before the TMA refill (async proxy) that the arrive below allows.  Without the fence the
+    // refill can land under a still-pending read when other kernels load the SMs (observed as
+    // a corrupted K slice with two streams running).
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + s);
   }
@@ -271,6 +294,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
                                                (size_t)T::CWARPS * T::RED_WARP * 8);
   uint64_t* empty = full + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) { tmap_acquire(&tmA); tmap_acquire(&tmB); }
   const int tx = (g.M + T::BM - 1) / T::BM, ty = (g.N + T::BN - 1) / T::BN;
   const bool red = T::RED && g.red_ok && g.beta == 1.0 && g.D2 == nullptr;
   unsigned red_chunk = 0;                      // this warp's staged chunks so far (buffer parity)
@@ -333,6 +357,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
   };
   if (producer)
     for (int i = 0; i < T::STAGES - 1; ++i) issue_next();
+  __syncwarp();
 
   const int wm = warp % T::WARPS_M, wn = warp / T::WARPS_M;
   const int fr = frag_row(lane >> 2), fc = lane & 3;
@@ -364,6 +389,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
     for (int kt = 0; kt < nk; ++kt, ++gstep) {
       const int s = gstep % T::STAGES;
       if (producer) issue_next();
+      __syncwarp();   // reconverge warp 0 (see gemm_tn_tma_kernel) before mma.sync.aligned
       mbar_wait(full + s, (gstep / T::STAGES) & 1);
       const double* sA = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES);
       const double* sB = reinterpret_cast<const double*>(base + (size_t)s * T::STAGE_BYTES + T::A_BYTES);
@@ -381,6 +407,7 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
 #pragma unroll
           for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
       }
+      fence_proxy_async_smem();   // WAR across proxies (see gemm_tn_tma_kernel)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
     }

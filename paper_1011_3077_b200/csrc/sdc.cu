@@ -105,6 +105,25 @@ struct sdc_handle {
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
   double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
+  // Second factorization context (lazy): its own stream and every buffer a QR / GRURV chain
+  // writes, so two independent chains run concurrently -- the left and right IRS of a
+  // pencil (Alg. 4), and in monitor mode GRURV(j) + similarity next to IRS pass j+1.
+  // swap_ctx() exchanges these fields with the active ones (host code is single-threaded).
+  struct Ctx {
+    cudaStream_t st = nullptr, st_hi = nullptr;
+    cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
+    double *Y = nullptr, *Yt = nullptr, *Tb = nullptr, *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr,
+           *Gb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr, *llbuf = nullptr,
+           *vec = nullptr, *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr, *C = nullptr, *G1 = nullptr,
+           *G2 = nullptr, *G3 = nullptr;
+    unsigned int* bar = nullptr;
+    unsigned long long bar_count = 0;
+    unsigned ll_epoch = 0;
+    int gemm_force = -1;
+  } alt;
+  int gemm_force = -1;   // debug: force a GEMM variant in this context
+  bool alt_ready = false, pipeline = true;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;   // cross-context dependencies
   // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
   struct GraphKey {
     int n = 0, max_iters = 0, nbo = 0, region = 0, rflags = 0;
@@ -157,6 +176,26 @@ int dalloc(sdc_handle* h, double** p, size_t elems) {
   *p = static_cast<double*>(q);
   return 0;
 }
+
+// exchange the active factorization context with h->alt
+void swap_ctx(sdc_handle* h) {
+  auto& a = h->alt;
+  std::swap(h->st, a.st); std::swap(h->st_hi, a.st_hi);
+  std::swap(h->la_fork, a.la_fork); std::swap(h->la_fac, a.la_fac);
+  std::swap(h->la_B, a.la_B); std::swap(h->la_join, a.la_join);
+  std::swap(h->Y, a.Y); std::swap(h->Yt, a.Yt); std::swap(h->Tb, a.Tb); std::swap(h->Tob, a.Tob);
+  std::swap(h->Tobt, a.Tobt); std::swap(h->Zb, a.Zb); std::swap(h->Gb, a.Gb); std::swap(h->tau, a.tau);
+  std::swap(h->Wp, a.Wp); std::swap(h->W, a.W); std::swap(h->gbuf, a.gbuf); std::swap(h->llbuf, a.llbuf);
+  std::swap(h->vec, a.vec); std::swap(h->Wp2, a.Wp2); std::swap(h->W2, a.W2); std::swap(h->Zb2, a.Zb2);
+  std::swap(h->bar, a.bar); std::swap(h->bar_count, a.bar_count); std::swap(h->ll_epoch, a.ll_epoch);
+  std::swap(h->C, a.C); std::swap(h->G1, a.G1); std::swap(h->G2, a.G2); std::swap(h->G3, a.G3);
+  std::swap(h->gemm_force, a.gemm_force);
+}
+struct AltScope {   // issue on the second context for the scope's lifetime
+  sdc_handle* h;
+  explicit AltScope(sdc_handle* h_) : h(h_) { swap_ctx(h); }
+  ~AltScope() { swap_ctx(h); }
+};
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline bool al16(const void* p, long long ld) {
@@ -314,9 +353,9 @@ template <class T>
 int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
                  const TmaGemmArgs& g, int splits) {
   static int attr_set = 0;
+  const int smem = (int)T::SMEM;
   if (!attr_set) {
-    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)T::SMEM));
+    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = 1;
   }
   CUtensorMap tA, tB, tC;
@@ -334,7 +373,7 @@ int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B,
   }
   dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
   ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
-  gemm_tn_tma_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, tC, g);
+  gemm_tn_tma_kernel<T><<<grid, T::THREADS, smem, h->st>>>(tA, tB, tC, g);
   SDC_LAUNCHED(h);
   return 0;
 }
@@ -343,9 +382,9 @@ template <class T>
 int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
                        const TmaGemmArgs& g, int splits) {
   static int attr_set = 0;
+  const int smem = (int)T::SMEM;
   if (!attr_set) {
-    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_persist_kernel<T>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM));
+    SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_persist_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set = 1;
   }
   CUtensorMap tA, tB;
@@ -356,7 +395,7 @@ int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const doub
   const long long tiles = (long long)cdiv(g.M, T::BM) * cdiv(g.N, T::BN) * splits;
   const int grid = (int)std::min<long long>(tiles, (long long)h->num_sms * T::MINB);
   ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
-  gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, T::SMEM, h->st>>>(tA, tB, g);
+  gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, smem, h->st>>>(tA, tB, g);
   SDC_LAUNCHED(h);
   return 0;
 }
@@ -391,7 +430,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (tma) {
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
                   (int)(al16(C, ldc) && M % 2 == 0), kupper};
-    int v = gemm_variant_override();
+    int v = h->gemm_force >= 0 ? h->gemm_force : gemm_variant_override();
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
       if (M <= 64) v = 1;
@@ -957,6 +996,70 @@ int reset_sync(sdc_handle* h) {
   SDC_CK(cudaMemsetAsync(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
   h->bar_count = 0;
   h->ll_epoch = 0;
+  if (h->alt_ready) {   // (on the caller's stream: ordered before any fork to the context)
+    SDC_CK(cudaMemsetAsync(h->alt.bar, 0, 64, h->st));
+    SDC_CK(cudaMemsetAsync(h->alt.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
+    h->alt.bar_count = 0;
+    h->alt.ll_epoch = 0;
+  }
+  return 0;
+}
+
+// allocate the second factorization context on first use (outside any graph capture)
+int ensure_alt(sdc_handle* h) {
+  if (h->alt_ready || !h->pipeline) return 0;
+  auto& a = h->alt;
+  const size_t n = (size_t)h->n_max, nn = n * n;
+  int rc = 0;
+#define ALLOC(p, e) \
+  if (!rc) rc = dalloc(h, &(p), (e))
+  ALLOC(a.Y, 2 * nn);
+  ALLOC(a.Yt, 2 * nn);
+  ALLOC(a.Tb, (n / NB + 1) * NB * NB);
+  ALLOC(a.Tob, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
+  ALLOC(a.Tobt, (n / h->nbo + 1) * (size_t)h->nbo * h->nbo);
+  ALLOC(a.Zb, (size_t)h->nbo * (n + 64));
+  ALLOC(a.Gb, (size_t)h->nbo * h->nbo);
+  ALLOC(a.tau, n + NB);
+  ALLOC(a.Wp, h->wp_elems);
+  ALLOC(a.W, (size_t)std::max(256, h->nbo) * (n + 64));
+  ALLOC(a.gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
+  ALLOC(a.llbuf, PANEL_LL_DOUBLES);
+  ALLOC(a.vec, 4 * n + 64);
+  ALLOC(a.C, 2 * nn);
+  ALLOC(a.G1, nn); ALLOC(a.G2, nn); ALLOC(a.G3, nn);
+  if (h->lookahead) {
+    ALLOC(a.Wp2, h->wp_elems);
+    ALLOC(a.W2, (size_t)std::max(256, h->nbo) * (n + 64));
+    ALLOC(a.Zb2, (size_t)h->nbo * (n + 64));
+  }
+#undef ALLOC
+  if (rc) return rc;
+  void* q = nullptr;
+  SDC_CK(cudaMalloc(&q, 64));
+  h->allocs.push_back(q);
+  a.bar = (unsigned*)q;
+  SDC_CK(cudaMemset(a.bar, 0, 64));
+  SDC_CK(cudaMemset(a.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)));
+  SDC_CK(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
+  if (h->lookahead) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    SDC_CK(cudaStreamCreateWithPriority(&a.st_hi, cudaStreamNonBlocking, greatest));
+    for (cudaEvent_t* e : {&a.la_fork, &a.la_fac, &a.la_B, &a.la_join})
+      SDC_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  for (cudaEvent_t* e : {&h->ev_a, &h->ev_b, &h->ev_c})
+    SDC_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  h->alt_ready = true;
+  return 0;
+}
+
+// make `to` wait for the work issued so far on `from` (fork / join between the contexts)
+int stream_dep(sdc_handle* h, cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+  (void)h;
+  SDC_CK(cudaEventRecord(ev, from));
+  SDC_CK(cudaStreamWaitEvent(to, ev, 0));
   return 0;
 }
 
@@ -1035,9 +1138,16 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
   const long long ld = n;
   const bool pencil = B != nullptr;
   if (!have_split) {
+    const bool two = pencil && !h->ql_orth && h->alt_ready;   // left GRURV on the second context
+    if (two) {
+      SDC_TRY(stream_dep(h, h->st, h->alt.st, h->ev_a));
+      AltScope as(h);
+      SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+    }
     SDC_TRY(grurv_right(h, n, h->A[cur], h->B[cur], h->Vt, Q, ldq));
     if (pencil && h->ql_orth) SDC_TRY(ql_from_aq(h, n, A, lda, Q, ldq, QLd, ld));
-    else if (pencil) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+    else if (pencil && !two) SDC_TRY(grurv_left(h, n, h->AL[cur], h->BL[cur], h->VLt, QLd, ld));
+    if (two) SDC_TRY(stream_dep(h, h->alt.st, h->st, h->ev_b));
     SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
   }
   SDC_TRY(norms(h, h->A[cur], ld, n, h->scal + 8));    // side indicator (res->side)
@@ -1053,6 +1163,10 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
                          cudaMemcpyDeviceToHost, h->st));
   SDC_CK(cudaMemcpyAsync(h->hflags, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   SDC_CK(cudaMemcpyAsync(h->hflags + 1, h->bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  if (h->alt_ready)
+    SDC_CK(cudaMemcpyAsync(h->hflags + 2, h->alt.bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+  else
+    h->hflags[2] = 0;
   return 0;
 }
 
@@ -1064,12 +1178,21 @@ int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const do
   const bool pencil = B != nullptr;
   SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, h->cur_V, h->cur_ldv, h->cur_VL, h->cur_ldvl));
   int cur = 0;
+  // Alg. 4: the right IRS on (A, B) and the left IRS on (A^T, B^T) are independent chains;
+  // with the second context they run concurrently (joined before the similarity)
+  const bool two = pencil && !h->ql_orth && h->alt_ready;
+  if (two) SDC_TRY(stream_dep(h, h->st, h->alt.st, h->ev_a));
   for (int j = 0; j < max_iters; ++j) {
     SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S, j,
                      nullptr, 0));
-    if (pencil && !h->ql_orth)
+    if (two) {
+      AltScope as(h);
       SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
                        h->SL, -1, nullptr, 0));
+    } else if (pencil && !h->ql_orth) {
+      SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
+                       h->SL, -1, nullptr, 0));
+    }
     cur ^= 1;
   }
   return enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, false, cur, max_iters);
@@ -1116,8 +1239,11 @@ void sdc_destroy(sdc_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
   if (h->st_hi) cudaStreamDestroy(h->st_hi);
-  for (cudaEvent_t e : {h->la_fork, h->la_fac, h->la_B, h->la_join})
+  for (cudaEvent_t e : {h->la_fork, h->la_fac, h->la_B, h->la_join, h->alt.la_fork, h->alt.la_fac,
+                        h->alt.la_B, h->alt.la_join, h->ev_a, h->ev_b, h->ev_c})
     if (e) cudaEventDestroy(e);
+  if (h->alt.st) cudaStreamDestroy(h->alt.st);
+  if (h->alt.st_hi) cudaStreamDestroy(h->alt.st_hi);
   if (h->hscal) cudaFreeHost(h->hscal);
   if (h->hflags) cudaFreeHost(h->hflags);
   for (void* p : h->allocs) cudaFree(p);
@@ -1243,6 +1369,9 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
   if (const char* e = getenv("SDC_LOOKAHEAD")) h->lookahead = atoi(e) != 0;
+  if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
+  if (const char* e = getenv("SDC_MAIN_GEMM")) h->gemm_force = atoi(e);
+  if (const char* e = getenv("SDC_ALT_GEMM")) h->alt.gemm_force = atoi(e);
   if (!rc && h->lookahead) {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
@@ -1575,6 +1704,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   if (Ahat && ldah < n) { set_err("ldah < n"); return -21; }
   if (hist_cap < 0 || (hist_cap > 0 && !hist)) { set_err("bad hist"); return -23; }
   if (!res) { set_err("res is NULL"); return -24; }
+  if (stop_mode == SDC_STOP_E21 || (pencil && !h->ql_orth)) SDC_TRY(ensure_alt(h));
   h->st = static_cast<cudaStream_t>(stream);
   h->cur_V = V; h->cur_ldv = ldv; h->cur_VL = VL; h->cur_ldvl = ldvl;
   const bool pencil_ = pencil;
@@ -1617,6 +1747,52 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     } else {
       SDC_TRY(enqueue_fixed(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, max_iters));
     }
+  } else if (stop_mode == SDC_STOP_E21 && h->alt_ready && !(pencil && !h->ql_orth)) {
+    // monitor mode, pipelined: GRURV(j) + similarity + selection of pass j run on the second
+    // context while IRS pass j+1 runs on the caller's stream (issued before the host reads
+    // pass j's metric; if pass j stops, that pass is discarded).  Same kernels on the same
+    // inputs as the sequential order, so the results are bit-identical to it.
+    const long long ld = n;
+    SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
+    int cur = 0;
+    bool have_split = false;
+    double prev = INFINITY;
+    SDC_TRY(irs_pass(h, n, h->A[0], ld, h->B[0], ld, h->A[1], ld, h->B[1], ld, h->S, 0, nullptr, 0));
+    for (int j = 0; j < max_iters; ++j) {
+      const int cj = cur ^ 1;   // buffers holding the output of pass j
+      if ((flags & SDC_FLAG_ONESIDED) && j >= 2) {
+        SDC_TRY(norms(h, h->A[cj], ld, n, h->scal + 8));
+        SDC_TRY(norms(h, h->B[cj], ld, n, h->scal + 10));
+        SDC_CK(cudaMemcpyAsync(h->hscal, h->scal + 8, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        SDC_CK(cudaStreamSynchronize(h->st));
+        const double fa = h->hscal[1], fb = h->hscal[3];
+        const double sd = fa + fb > 0.0 ? fb / (fa + fb) : 0.5;
+        if (sd < 1e-6 || sd > 1.0 - 1e-6) { cur = cj; p = j + 1; break; }
+      }
+      SDC_TRY(stream_dep(h, h->st, h->alt.st, h->ev_a));
+      {
+        AltScope as(h);
+        SDC_TRY(grurv_right(h, n, h->A[cj], h->B[cj], h->Vt, Q, ldq));
+        if (pencil) SDC_TRY(ql_from_aq(h, n, A, lda, Q, ldq, QLd, ld));
+        SDC_TRY(similarity_select(h, n, A, lda, B, ldb, Q, ldq, pencil ? QLd : Q, pencil ? ld : ldq));
+        SDC_CK(cudaMemcpyAsync(h->hscal + 16, h->scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+        SDC_CK(cudaEventRecord(h->ev_b, h->st));
+      }
+      have_split = true;
+      // next pass (reads pass j's output, overwrites pass j-1's, whose GRURV has completed)
+      if (j + 1 < max_iters)
+        SDC_TRY(irs_pass(h, n, h->A[cj], ld, h->B[cj], ld, h->A[cur], ld, h->B[cur], ld, h->S, j + 1,
+                         nullptr, 0));
+      cur = cj;
+      SDC_CK(cudaEventSynchronize(h->ev_b));
+      const double r_j = h->hscal[16], m_j = h->hscal[17];
+      if (j < hist_cap) { hbuf[3 * j] = r_j; hbuf[3 * j + 1] = m_j; }
+      if (m_j <= tol) { p = j + 1; conv = 1; break; }
+      if ((flags & SDC_FLAG_PLATEAU) && m_j <= 10.0 * tol && m_j > 0.5 * prev) { p = j + 1; conv = 1; break; }
+      prev = m_j;
+    }
+    SDC_TRY(stream_dep(h, h->alt.st, h->st, h->ev_c));
+    SDC_TRY(enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, have_split, cur, max_iters));
   } else {
     // RTEST / E21: host decisions between passes (one scalar D2H per pass)
     const long long ld = n;
@@ -1666,7 +1842,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     SDC_TRY(enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, have_split, cur, max_iters));
   }
   SDC_CK(cudaStreamSynchronize(h->st));
-  if (h->hflags[1]) { set_err("panel grid barrier timed out (co-residency violated?)"); return SDC_ERR_CUDA; }
+  if (h->hflags[1] || h->hflags[2]) { set_err("panel grid barrier timed out (co-residency violated?)"); return SDC_ERR_CUDA; }
   const double* sc = h->hscal;
   for (int j = 1; j < std::min(hist_cap, p); ++j) hbuf[3 * j + 2] = sc[SCAL_HIST + j];
   if (hist_cap > 0) memcpy(hist, hbuf.data(), sizeof(double) * hbuf.size());

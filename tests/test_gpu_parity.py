@@ -322,6 +322,26 @@ def test_lookahead_graph_replay_matches_direct(sdc):
     assert ig1.metric == ig2.metric == idd.metric and ig1.r == idd.r
 
 
+@pytest.mark.parametrize("cfg,n", [(3, 700), (4, 300)])
+def test_second_context_bit_identical(sdc, cfg, n):
+    # monitor mode with GRURV(j) on the second context next to IRS pass j+1 (config 3), and
+    # the pencil's left IRS / left GRURV concurrent with the right ones (config 4): same
+    # kernels on the same inputs as the single-stream order -> bit-identical outputs
+    p = inputs.make_config(cfg, n=n)
+    outs = []
+    for pipe in (0, 1):
+        h = _handle_with_env(sdc, n, pencil=p.B is not None, SDC_PIPELINE=pipe)
+        Bd = None if p.B is None else dev(p.B)
+        VLd = None if p.VL is None else dev(p.VL)
+        Q, QL, Ah, info = h.split(dev(p.A), Bd, dev(p.V), VLd, max_iters=p.max_iters, tol=p.tol,
+                                  stop={0: "fixed", 1: "rtest", 2: "e21"}[p.stop], want_ahat=True)
+        outs.append((Q, QL, Ah, info))
+    (q0, l0, a0, i0), (q1, l1, a1, i1) = outs
+    assert torch.equal(q0, q1) and torch.equal(a0, a1)
+    assert (l0 is None) == (l1 is None) and (l0 is None or torch.equal(l0, l1))
+    assert (i0.k, i0.r, i0.iters, i0.metric, i0.status) == (i1.k, i1.r, i1.iters, i1.metric, i1.status)
+
+
 def test_blocked_qr_two_level_r_unique(orc, sdc):
     # R of the two-level QR equals the oracle's (unique with diag >= 0) at 2n x n, n = 700
     h = _handle_with_env(sdc, 700, SDC_NBO=256)
