@@ -342,6 +342,20 @@ def test_second_context_bit_identical(sdc, cfg, n):
     assert (i0.k, i0.r, i0.iters, i0.metric, i0.status) == (i1.k, i1.r, i1.iters, i1.metric, i1.status)
 
 
+@pytest.mark.parametrize("rows", [64, 128, 256])
+@pytest.mark.parametrize("m,n", [(2048, 1024), (1000, 997), (4096, 300), (129, 64), (70, 70)])
+def test_panel_variants_r_unique(orc, sdc, rows, m, n):
+    # panels at every rows-per-CTA tier (register variants RPT 8/16/32) give the unique
+    # diag >= 0 R of the oracle and an orthogonal Q at ragged sizes
+    h = _handle_with_env(sdc, max(m, n), SDC_PANEL_ROWS=rows)
+    s = np.random.default_rng(m * 3 + n).standard_normal((m, n))
+    q, r = h.qr(dev(s))
+    _, r_o = orc.qr_signed(s)
+    assert np.allclose(host(r), r_o, rtol=0, atol=1e-12 * np.abs(r_o).max() * np.sqrt(n))
+    assert orth_err(host(q)) <= 64 * n * EPS
+    assert np.linalg.norm(host(q) @ host(r) - s) <= 64 * n * EPS * np.linalg.norm(s)
+
+
 def test_blocked_qr_two_level_r_unique(orc, sdc):
     # R of the two-level QR equals the oracle's (unique with diag >= 0) at 2n x n, n = 700
     h = _handle_with_env(sdc, 700, SDC_NBO=256)
@@ -370,7 +384,8 @@ def test_graph_replay_matches_direct(sdc):
     assert hg.launches > 0
 
 
-@pytest.mark.parametrize("env", [{"SDC_NO_CLUSTER": 1}, {"SDC_CLUSTER_MAX_ROWS": 4096}])
+@pytest.mark.parametrize("env", [{"SDC_NO_CLUSTER": 1}, {"SDC_CLUSTER_MAX_ROWS": 4096},
+                                 {"SDC_PANEL_ROWS": 64}, {"SDC_PANEL_ROWS": 256}])
 def test_panel_exchange_modes_parity(orc, sdc, env):
     # cluster/DSMEM panel (small panels) and cooperative-grid/L2 panel give the same
     # invariants on config 2's recipe at n = 600
