@@ -254,9 +254,12 @@ int sdc_split_select(sdc_handle* h, void* stream, int n, const double* Ahat, int
 /* Per-kernel-class timing with CUDA events recorded on the launching stream around every
  * launch of the class (measurement support for bench.py's roofline numbers).
  * sdc_profile(h, 1) resets the counters and starts recording, (h, 0) stops.
- * sdc_profile_read returns, for class cls, the summed event time (ms), the number of
- * launches and the summed ALGORITHMIC work: flops 2MNK for SDC_PROF_GEMM, bytes
- * (read + write of the operands the definition touches) for the other classes. */
+ * sdc_profile_read returns, for class cls, the class time (ms), the number of launches
+ * and the summed ALGORITHMIC work: flops 2MNK for SDC_PROF_GEMM, bytes (read + write of
+ * the operands the definition touches) for the other classes.  The class time is the
+ * UNION of the launch intervals, i.e. the wall time during which at least one launch of the
+ * class ran.  Launches of a class can overlap on the look-ahead and second-context streams;
+ * on a serial schedule the union equals the summed durations. */
 enum { SDC_PROF_GEMM = 0,        /* every DMMA GEMM launch                                */
        SDC_PROF_PANEL = 1, SDC_PROF_WYRED = 2, SDC_PROF_SELECT = 3,
        SDC_PROF_GEMM_W0 = 4,     /* subset of GEMM: split-K W0 = Y^T C of WY applications    */

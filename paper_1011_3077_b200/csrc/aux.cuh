@@ -116,6 +116,28 @@ __global__ void k_place_ahat(double* T, long long ldt, const double* Ah, long lo
 //   mode 1: out(i,j) = src(n-1-j, i)                  (C^T J)
 //   mode 2: out(i,j) = src(n-1-i, n-1-j)              (J X J, no transpose)
 //   mode 3: out(i,j) = src(n-1-i, j)                  (J X, row reversal)
+// out1 = out2 = rho * src^T (n x n).  The first IRS pass of an RNEP step has B_0 = rho I, so
+// B_1 = Q22^T B_0 = rho Q22^T: the product with the identity is a scaled transpose (the same
+// values the GEMM would produce: every other term of its dot products is an exact zero).
+__global__ void k_transpose_scale2(double* out1, long long ld1, double* out2, long long ld2,
+                                   const double* src, long long lds, int n, double rho) {
+  __shared__ double tile[32][33];
+  const int bi = blockIdx.x * 32, bj = blockIdx.y * 32, tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    const int sr = bj + tx, sc = bi + r;
+    if (sr < n && sc < n) tile[r][tx] = src[sr + (long long)sc * lds];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi + tx, j = bj + r;
+    if (i < n && j < n) {
+      const double v = rho * tile[tx][r];
+      out1[i + (long long)j * ld1] = v;
+      out2[i + (long long)j * ld2] = v;
+    }
+  }
+}
+
 __global__ void k_transpose_rev(double* out, long long ldo, const double* src, long long lds, int n,
                                 int mode) {
   __shared__ double tile[32][33];

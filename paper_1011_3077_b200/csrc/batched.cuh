@@ -305,4 +305,293 @@ __global__ void __launch_bounds__(BAT_THREADS, 1) k_split_batched(const BatArgs 
   }
 }
 
+// =======================================================================================
+// Compact-WY variant (default): the same step with every O(n^3) contraction on the FP64
+// tensor cores (mma.sync m8n8k4 DMMA on shared-memory operands) and 2 CTA barriers per
+// Householder column instead of ~5:
+//   QR (bq_qr): reflector columns stay UNSCALED during the factorisation (v_k = sc_k x_k),
+//     one pass of column dot products g_j = x_k^T P(:, j) per column gives the norm, the
+//     update coefficients and the Gram entries of the compact-WY T column (PAPER.md:331's
+//     "QR", LAPACK dgeqr2 + dlarft arithmetic in a blocked order);
+//   IRS pass (Alg. 3): with Q = I - Y T Y^T and the complement C = Q [0; I] = [0; I] - Y Z,
+//     Z = T Y2^T (Y2 = rows n..2n-1 of Y), the products need no explicit C:
+//     A_{j+1} = C1^T A_j = -Z^T (Y1^T A_j),  B_{j+1} = C2^T B_j = B_j - Z^T (Y2^T B_j);
+//   GRURV: QR(A_p V^T) -> U^T (A_p + B_p) = S - Y T^T (Y^T S), row signs, RQ as the QR of
+//     C^T J with explicit Q_qr = I - Y (T Y^T), Q = Q_qr D J (reading Q10);
+//   similarity Q^T A Q with the original A, selection as above.
+// All matrices live in shared memory with leading dimension NP = n rounded up to 16 (2 NP for
+// the stack) and zero padding; accessors return 0 outside the logical ranges.
+// =======================================================================================
+constexpr int BQ_THREADS = 512;
+
+struct BqShape { int n, m, np; };
+
+// out(i, j) (16x16 warp tiles over P_ x Q_) = sum_k fa(i, k) fb(k, j), then fo(i, j, v)
+template <class FA, class FB, class FO>
+SDC_DEV void bq_mma(int P_, int Q_, int K_, FA fa, FB fb, FO fo) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int tm = P_ / 16, tn = Q_ / 16;
+  for (int tile = warp; tile < tm * tn; tile += BQ_THREADS / 32) {
+    const int i0 = (tile % tm) * 16, j0 = (tile / tm) * 16;
+    double acc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+    for (int k0 = 0; k0 < K_; k0 += 4) {
+      double a[2], b[2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) a[mi] = fa(i0 + mi * 8 + g, k0 + t);
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni) b[ni] = fb(k0 + t, j0 + ni * 8 + g);
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) dmma_8x8x4(acc[mi][ni], a[mi], b[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) fo(i0 + mi * 8 + g, j0 + ni * 8 + 2 * t + hh, acc[mi][ni][hh]);
+  }
+  __syncthreads();
+}
+
+// unscaled Householder QR of the m x n P (ld ldp) with compact-WY T (NP x NP, ld np, upper):
+// on exit P holds x_k below the diagonal (v_k = sc[k] x_k, unit diagonal implied), R above,
+// beta[k] = R(k, k); I - Y T Y^T = H_0 ... H_{n-1}.  Two CTA barriers per column.
+SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* sc, double* tau,
+                   double* beta, double* g) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < np * np; e += BQ_THREADS) T[e] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    // (A) g_j = sum_{r > k} x_k(r) P(r, j), every column j (j < k: Gram entries for T)
+    for (int j = warp; j < n; j += BQ_THREADS / 32) {
+      double s = 0.0;
+      for (int r = k + 1 + lane; r < m; r += 32) s = fma(P[r + k * ldp], P[r + j * ldp], s);
+      s = warp_sum(s);
+      if (lane == 0) g[j] = s;
+    }
+    __syncthreads();
+    // (B) reflector (dlarfg, Q7), identical in every thread
+    const double alpha = P[k + k * ldp], sigma = g[k];
+    double tk = 0.0, scale = 0.0, bk = alpha;
+    if (sigma != 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, sigma));
+      bk = alpha < 0.0 ? nrm : -nrm;
+      tk = (bk - alpha) / bk;
+      scale = 1.0 / (alpha - bk);
+    }
+    for (int j = k + 1 + warp; j < n; j += BQ_THREADS / 32) {   // columns j > k
+      const double w = tk * fma(scale, g[j], P[k + j * ldp]);
+      const double ws = w * scale;
+      for (int r = k + 1 + lane; r < m; r += 32) P[r + j * ldp] = fma(-ws, P[r + k * ldp], P[r + j * ldp]);
+      __syncwarp();
+      if (lane == 0) P[k + j * ldp] -= w;
+    }
+    // T(0:k, k) = -tau_k T(0:k, 0:k) g',  g'_l = sc_l (x_l(k) + scale g_l);  T(k, k) = tau_k
+    {
+      const int i = tid >> 2, q = tid & 3;
+      double acc = 0.0;
+      if (i < k)
+        for (int l = i + q; l < k; l += 4) acc = fma(T[i + l * np], sc[l] * fma(scale, g[l], P[k + l * ldp]), acc);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (i < k && q == 0) T[i + k * np] = -tk * acc;
+      if (tid == 0) {
+        T[k + k * np] = tk;
+        sc[k] = scale;
+        tau[k] = tk;
+        beta[k] = bk;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArgs a) {
+  extern __shared__ __align__(16) double smq[];
+  const int n = a.n, m = 2 * n, b = blockIdx.x, tid = threadIdx.x;
+  const int np = (n + 15) & ~15, NN = np * np, ldp = 2 * np;
+  double* Aj = smq;                 // np x np
+  double* Bj = Aj + NN;
+  double* P = Bj + NN;              // 2np x np: stack / factored matrices
+  double* T = P + 2 * NN;           // np x np
+  double* Z = T + NN;
+  double* W = Z + NN;
+  double* sc = W + NN;              // np
+  double* tau = sc + np;
+  double* beta = tau + np;
+  double* g = beta + np;            // np
+  double* msel = g + np;            // np
+  double* red = msel + np;          // 2 * BAT_WARPS + 16
+  const double* A0 = a.A + (long long)b * a.sa;
+  const double* V0 = a.V + (long long)b * a.sv;
+
+  for (int e = tid; e < NN; e += BQ_THREADS) {
+    const int i = e % np, j = e / np;
+    const bool in = i < n && j < n;
+    Aj[e] = in ? A0[i + (long long)j * a.lda] : 0.0;
+    Bj[e] = (in && i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  double nA = 0.0, fA;
+  {
+    double f = 0.0;
+    for (int e = tid; e < NN; e += BQ_THREADS) f += Aj[e] * Aj[e];
+    fA = sqrt(bat_sum(f, red));
+    if (tid < n) {
+      double c = 0.0;
+      for (int i = 0; i < n; ++i) c += fabs(Aj[i + tid * np]);
+      msel[tid] = c;
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) nA = fmax(nA, msel[j]);
+    __syncthreads();
+  }
+  // implicit unit-lower Y of the last factorisation of P (rows m_, columns n)
+  auto Yv = [&](int r, int k, int m_) -> double {
+    if (k >= n || r >= m_ || r < k) return 0.0;
+    return r == k ? 1.0 : sc[k] * P[r + k * ldp];
+  };
+
+  // ---- IRS passes (Alg. 3) -----------------------------------------------------------
+  for (int pass = 0; pass < a.passes; ++pass) {
+    for (int e = tid; e < 2 * NN; e += BQ_THREADS) {   // P = [B_j; -A_j] (rows >= 2n zero)
+      const int i = e % ldp, j = e / ldp;
+      double v = 0.0;
+      if (j < n) v = i < n ? Bj[i + j * np] : (i < m ? -Aj[(i - n) + j * np] : 0.0);
+      P[e] = v;
+    }
+    __syncthreads();
+    bq_qr(m, n, np, P, ldp, T, sc, tau, beta, g);
+    // Z = T Y2^T
+    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * np]; },
+           [&](int k, int j) { return Yv(n + j, k, m); },
+           [&](int i, int j, double v) { Z[i + j * np] = v; });
+    // W = Y1^T A_j ;  A_{j+1} = -Z^T W
+    bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
+           [&](int k, int j) { return Aj[k + j * np]; },
+           [&](int i, int j, double v) { W[i + j * np] = v; });
+    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * np]; },
+           [&](int k, int j) { return W[k + j * np]; },
+           [&](int i, int j, double v) { Aj[i + j * np] = -v; });
+    // W = Y2^T B_j ;  B_{j+1} = B_j - Z^T W
+    bq_mma(np, np, np, [&](int i, int k) { return Yv(n + k, i, m); },
+           [&](int k, int j) { return Bj[k + j * np]; },
+           [&](int i, int j, double v) { W[i + j * np] = v; });
+    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * np]; },
+           [&](int k, int j) { return W[k + j * np]; },
+           [&](int i, int j, double v) { Bj[i + j * np] -= v; });
+  }
+
+  // ---- GRURV(2, A_p + B_p, A_p; -1, +1) ------------------------------------------------
+  // X = A_p V^T into P (ld 2np)
+  bq_mma(np, np, np, [&](int i, int k) { return Aj[i + k * np]; },
+         [&](int k, int j) { return (k < n && j < n) ? V0[j + (long long)k * a.ldv] : 0.0; },
+         [&](int i, int j, double v) { P[i + j * ldp] = v; });
+  bq_qr(n, n, np, P, ldp, T, sc, tau, beta, g);                   // X = U R_2
+  for (int e = tid; e < NN; e += BQ_THREADS) Aj[e] += Bj[e];       // S = A_p + B_p
+  __syncthreads();
+  // U^T S = S - Y T^T (Y^T S)
+  bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
+         [&](int k, int j) { return Aj[k + j * np]; },
+         [&](int i, int j, double v) { W[i + j * np] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return T[k + i * np]; },
+         [&](int k, int j) { return W[k + j * np]; },
+         [&](int i, int j, double v) { Z[i + j * np] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
+         [&](int k, int j) { return Z[k + j * np]; },
+         [&](int i, int j, double v) {
+           const double s = Aj[i + j * np] - v;
+           Aj[i + j * np] = (i < n && beta[i] < 0.0) ? -s : s;     // U <- U D_U
+         });
+  // M = C^T J into P: M(i, j) = C(n-1-j, i)
+  for (int e = tid; e < 2 * NN; e += BQ_THREADS) {
+    const int i = e % ldp, j = e / ldp;
+    P[e] = (i < n && j < n) ? Aj[(n - 1 - j) + i * np] : 0.0;
+  }
+  __syncthreads();
+  bq_qr(n, n, np, P, ldp, T, sc, tau, beta, g);
+  // Q_qr = I - Y (T Y^T):  W = T Y^T, Z = I - Y W
+  bq_mma(np, np, np, [&](int i, int k) { return T[i + k * np]; },
+         [&](int k, int j) { return Yv(j, k, n); },
+         [&](int i, int j, double v) { W[i + j * np] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
+         [&](int k, int j) { return W[k + j * np]; },
+         [&](int i, int j, double v) { Z[i + j * np] = (i == j && i < n ? 1.0 : 0.0) - v; });
+  // Q(:, j) = sign(R(jj, jj)) Q_qr(:, jj), jj = n-1-j  -> Bj
+  for (int e = tid; e < NN; e += BQ_THREADS) {
+    const int i = e % np, j = e / np;
+    double v = 0.0;
+    if (i < n && j < n) {
+      const int jj = n - 1 - j;
+      v = (beta[jj] < 0.0 ? -1.0 : 1.0) * Z[i + jj * np];
+    }
+    Bj[e] = v;
+  }
+  __syncthreads();
+
+  // ---- similarity Ahat = Q^T A Q (original A), split selection ------------------------------
+  bq_mma(np, np, np, [&](int i, int k) { return (i < n && k < n) ? A0[i + (long long)k * a.lda] : 0.0; },
+         [&](int k, int j) { return Bj[k + j * np]; },
+         [&](int i, int j, double v) { W[i + j * np] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Bj[k + i * np]; },
+         [&](int k, int j) { return W[k + j * np]; },
+         [&](int i, int j, double v) { Aj[i + j * np] = v; });
+  // suffix column sums: Z[c + r np] = sum_{i >= r} |Ahat(i, c)| for c < r
+  if (tid < n) {
+    double s = 0.0;
+    for (int r = n - 1; r >= 1; --r) {
+      s += fabs(Aj[r + tid * np]);
+      Z[tid + r * np] = s;
+    }
+  }
+  __syncthreads();
+  if (tid >= 1 && tid < n) {
+    const int r = tid;
+    double ma = 0.0;
+    for (int c = 0; c < r; ++c) {
+      const double v = Z[c + r * np];
+      if (v > ma || v != v) ma = v;
+    }
+    msel[r] = ma / nA;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int best = 1;
+    for (int r = 2; r <= n - 1; ++r)
+      if (msel[r] < msel[best]) best = r;
+    red[2 * BAT_WARPS] = best;
+    red[2 * BAT_WARPS + 1] = msel[best];
+  }
+  __syncthreads();
+  const int rbest = (int)red[2 * BAT_WARPS];
+  double f = 0.0, nf = 0.0;
+  for (int e = tid; e < NN; e += BQ_THREADS) {
+    const int i = e % np, j = e / np;
+    if (i >= n || j >= n) continue;
+    const double v = Aj[e];
+    if (i >= rbest && j < rbest) f += v * v;
+    if (!(fabs(v) <= 1.79e308)) nf = 1.0;
+  }
+  const double e21f = sqrt(bat_sum(f, red));
+  const double nonfinite = bat_sum(nf, red);
+  double* Qo = a.Q + (long long)b * a.sq;
+  for (int e = tid; e < n * n; e += BQ_THREADS) {
+    const int i = e % n, j = e / n;
+    Qo[i + (long long)j * a.ldq] = Bj[i + j * np];
+  }
+  if (tid == 0) {
+    a.out[4 * b + 0] = rbest;
+    a.out[4 * b + 1] = red[2 * BAT_WARPS + 1];
+    a.out[4 * b + 2] = e21f / fA;
+    a.out[4 * b + 3] = nonfinite;
+  }
+}
+
+inline size_t bq_smem_bytes(int n) {
+  const size_t np = (size_t)((n + 15) & ~15);
+  return sizeof(double) * (7 * np * np + 5 * np + 2 * BAT_WARPS + 16);
+}
+
 }  // namespace sdc

@@ -146,6 +146,8 @@ struct sdc_handle {
   const double *cur_V = nullptr, *cur_VL = nullptr;
   int region = SDC_REGION_UNIT_DISK, rflags = 0;   // region / flags of the current call
   double rparam = 1.0;
+  const double* b_ident = nullptr;     // B buffer known to hold b_ident_rho * I (first pass)
+  double b_ident_rho = 1.0;
   long long cur_ldv = 0, cur_ldvl = 0;
   unsigned int* hflags = nullptr;      // pinned: [0] non-finite flag, [1] barrier error
   // optional per-kernel-class timing with CUDA events on the launching stream
@@ -240,15 +242,33 @@ struct ProfScope {
     }
   }
 };
+// Launches of one class can overlap (look-ahead QR, second context), so the class time is
+// the UNION of its launch intervals -- the wall time during which at least one launch of the
+// class ran -- not the sum of durations; for a serial schedule the two are equal.
 void prof_collect(sdc_handle* h) {
   if (h->recs.empty()) return;
-  for (auto& r : h->recs) {   // events may sit on two streams (look-ahead QR): wait for each
-    cudaEventSynchronize(h->ev_pool[r.e1]);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev_pool[r.e0], h->ev_pool[r.e1]);
-    h->prof_ms[r.cls] += ms;
+  for (auto& r : h->recs) cudaEventSynchronize(h->ev_pool[r.e1]);   // events on several streams
+  const cudaEvent_t ref = h->ev_pool[h->recs.front().e0];
+  std::vector<std::pair<float, float>> iv[SDC_PROF_CLASSES];
+  for (auto& r : h->recs) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ref, h->ev_pool[r.e0]);
+    cudaEventElapsedTime(&b, ref, h->ev_pool[r.e1]);
+    iv[r.cls].push_back({a, b});
     h->prof_work[r.cls] += r.work;
     h->prof_n[r.cls] += 1;
+  }
+  for (int c = 0; c < SDC_PROF_CLASSES; ++c) {
+    auto& v = iv[c];
+    if (v.empty()) continue;
+    std::sort(v.begin(), v.end());
+    double tot = 0.0, lo = v[0].first, hi = v[0].second;
+    for (size_t i = 1; i < v.size(); ++i) {
+      if (v[i].first > hi) { tot += hi - lo; lo = v[i].first; hi = v[i].second; }
+      else hi = std::max(hi, (double)v[i].second);
+    }
+    tot += hi - lo;
+    h->prof_ms[c] += tot;
   }
   h->recs.clear();
   h->ev_used = 0;
@@ -875,6 +895,13 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
   SDC_TRY(apply_q(h, (int)m, n, f, h->C, m, n));
   // A_{j+1} = Q12^T A_j (-> next stack lower half, negated); B_{j+1} = Q22^T B_j (upper)
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C, m, Aj, lda, 0.0, An, ldan, S + n, m, -1.0));
+  if (Bj != nullptr && Bj == h->b_ident) {   // B_j = rho I (first RNEP pass): B_{j+1} = rho Q22^T
+    h->b_ident = nullptr;
+    dim3 grid(cdiv(n, 32), cdiv(n, 32));
+    k_transpose_scale2<<<grid, dim3(32, 8), 0, h->st>>>(Bn, ldbn, S, m, h->C + n, m, n, h->b_ident_rho);
+    SDC_LAUNCHED(h);
+    return 0;
+  }
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C + n, m, Bj, ldb, 0.0, Bn, ldbn, S, m, 1.0));
   return 0;
 }
@@ -1095,6 +1122,7 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
   const long long ld = n, m = 2LL * n;
   const bool pencil = B != nullptr;
   SDC_TRY(reset_sync(h));
+  h->b_ident = nullptr;
   SDC_CK(cudaMemsetAsync(h->Rprev, 0, sizeof(double) * (size_t)n * n, h->st));
   SDC_TRY(norms(h, A, lda, n, h->scal));
   if (pencil) SDC_TRY(norms(h, B, ldb, n, h->scal + 2));
@@ -1113,6 +1141,8 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
     k_copy<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, B, ldb, n, n, rho);
   } else {
     k_set_identity<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->B[0], ld, n, n, rho);
+    h->b_ident = h->B[0];
+    h->b_ident_rho = rho;
   }
   SDC_LAUNCHED(h);
   k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, h->A[0], ld, h->B[0], ld, n);
@@ -1550,10 +1580,14 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
   if (batch == 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->st = st;
-  const size_t smem = bat_smem_doubles() * sizeof(double);
+  static const bool v1 = getenv("SDC_BATCHED_V1") != nullptr;   // unblocked variant (A/B)
+  const size_t smem = v1 ? bat_smem_doubles() * sizeof(double) : bq_smem_bytes(BAT_NMAX);
   static bool attr = false;
   if (!attr) {
-    SDC_CK(cudaFuncSetAttribute(k_split_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SDC_CK(cudaFuncSetAttribute(k_split_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(bat_smem_doubles() * sizeof(double))));
+    SDC_CK(cudaFuncSetAttribute(k_split_batched_wy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)bq_smem_bytes(BAT_NMAX)));
     attr = true;
   }
   if ((size_t)batch * 4 > h->bat_out_n) {
@@ -1567,7 +1601,8 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
     h->bat_out_n = (size_t)batch * 4;
   }
   BatArgs a{A, lda, strideA, V, ldv, strideV, Q, ldq, strideQ, h->bat_out, n, max_iters};
-  k_split_batched<<<batch, BAT_THREADS, smem, st>>>(a);
+  if (v1) k_split_batched<<<batch, BAT_THREADS, smem, st>>>(a);
+  else k_split_batched_wy<<<batch, BQ_THREADS, bq_smem_bytes(n), st>>>(a);
   SDC_LAUNCHED(h);
   std::vector<double> out((size_t)batch * 4);
   SDC_CK(cudaMemcpyAsync(out.data(), h->bat_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1937,6 +1972,7 @@ int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, c
   SDC_TRY(reset_sync(h));
   k_build_stack<<<ew_grid(m * n), 256, 0, h->st>>>(h->S, m, A, lda, B, ldb, n);
   SDC_LAUNCHED(h);
+  h->b_ident = nullptr;
   SDC_TRY(irs_pass(h, n, A, lda, B, ldb, Aout, ldao, Bout, ldbo, h->S, -1, Rout, ldr));
   SDC_TRY(check_barrier(h));
   return 0;
