@@ -469,14 +469,26 @@ __global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits,
   const int c0 = blockIdx.x * cpb;
   const int elems = cpb * nb;
   const int g = elems >= (int)blockDim.x ? 1 : (int)blockDim.x / elems;
+  // partial sums over the split slices z = q0, q0 + dz, ...: 4 independent accumulators
+  // (loads in flight together; the split count reaches ~150 for tall panels), combined in
+  // a fixed order
+  auto slice_sum = [&](const double* p, int q0, int dz) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int z = q0;
+    for (; z + 3 * dz < splits; z += 4 * dz) {
+      s0 += p[(long long)z * zstride];
+      s1 += p[(long long)(z + dz) * zstride];
+      s2 += p[(long long)(z + 2 * dz) * zstride];
+      s3 += p[(long long)(z + 3 * dz) * zstride];
+    }
+    for (; z < splits; z += dz) s0 += p[(long long)z * zstride];
+    return (s0 + s1) + (s2 + s3);
+  };
   if (g == 1) {
     for (int e = threadIdx.x; e < elems; e += blockDim.x) {
       const int c = c0 + e / nb;
       double s = 0.0;
-      if (c < ncols) {
-        const double* p = Wp + (e % nb) + (long long)c * nb;
-        for (int z = 0; z < splits; ++z) s += p[(long long)z * zstride];
-      }
+      if (c < ncols) s = slice_sum(Wp + (e % nb) + (long long)c * nb, 0, 1);
       w0[e] = s;
     }
   } else {
@@ -484,10 +496,7 @@ __global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits,
     if (q < g) {
       const int c = c0 + e / nb;
       double s = 0.0;
-      if (c < ncols) {
-        const double* p = Wp + (e % nb) + (long long)c * nb;
-        for (int z = q; z < splits; z += g) s += p[(long long)z * zstride];
-      }
+      if (c < ncols) s = slice_sum(Wp + (e % nb) + (long long)c * nb, q, g);
       part[q * elems + e] = s;
     }
     __syncthreads();
@@ -516,9 +525,16 @@ __global__ void __launch_bounds__(256) k_wy_reduce(const double* Wp, int splits,
 __global__ void k_sum_partials(const double* P, int splits, long long zs, long long total, double* Z) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += P[(long long)z * zs + e];
-    Z[e] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;   // 4 loads in flight, fixed combine order
+    int z = 0;
+    for (; z + 3 < splits; z += 4) {
+      s0 += P[(long long)z * zs + e];
+      s1 += P[(long long)(z + 1) * zs + e];
+      s2 += P[(long long)(z + 2) * zs + e];
+      s3 += P[(long long)(z + 3) * zs + e];
+    }
+    for (; z < splits; ++z) s0 += P[(long long)z * zs + e];
+    Z[e] = (s0 + s1) + (s2 + s3);
   }
 }
 
