@@ -102,6 +102,8 @@ struct sdc_handle {
   // handle stream, the bulk trailing update of each outer block on the caller's stream with
   // its own split-K workspace (Wp2, W2, Zb2)
   bool lookahead = true;
+  bool on_side = false;                // issuing on the look-ahead side stream
+  int side_reserve = 0;                // SMs the side stream's persistent GEMMs leave free
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
   double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
@@ -413,7 +415,11 @@ int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const doub
     return SDC_ERR_CUDA;
   }
   const long long tiles = (long long)cdiv(g.M, T::BM) * cdiv(g.N, T::BN) * splits;
-  const int grid = (int)std::min<long long>(tiles, (long long)h->num_sms * T::MINB);
+  // on the look-ahead side stream the persistent CTAs leave side_reserve SMs to the
+  // critical chain (panels, next-block updates), whose kernels would otherwise queue behind
+  // CTAs that do not retire until the whole update is done
+  const int sms = h->on_side ? std::max(1, h->num_sms - h->side_reserve) : h->num_sms;
+  const int grid = (int)std::min<long long>(tiles, (long long)sms * T::MINB);
   ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
   gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, smem, h->st>>>(tA, tB, g);
   SDC_LAUNCHED(h);
@@ -745,6 +751,7 @@ struct LaScope {   // restores the caller's stream and the primary workspace on 
   explicit LaScope(sdc_handle* h_) : h(h_), side(h_->st) {}
   void use_side(bool on) {
     h->st = on ? side : h->st_hi;
+    h->on_side = on;
     if ((h->Wp2 != nullptr) && on != swapped) {
       std::swap(h->Wp, h->Wp2); std::swap(h->W, h->W2); std::swap(h->Zb, h->Zb2);
       swapped = on;
@@ -754,6 +761,7 @@ struct LaScope {   // restores the caller's stream and the primary workspace on 
   ~LaScope() {
     if (swapped) { std::swap(h->Wp, h->Wp2); std::swap(h->W, h->W2); std::swap(h->Zb, h->Zb2); }
     h->st = side;
+    h->on_side = false;
   }
 };
 
@@ -1399,6 +1407,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
   if (const char* e = getenv("SDC_LOOKAHEAD")) h->lookahead = atoi(e) != 0;
+  if (const char* e = getenv("SDC_SIDE_RESERVE")) h->side_reserve = std::max(0, atoi(e));
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
   if (const char* e = getenv("SDC_MAIN_GEMM")) h->gemm_force = atoi(e);
   if (const char* e = getenv("SDC_ALT_GEMM")) h->alt.gemm_force = atoi(e);
