@@ -118,7 +118,9 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   // the address space visible to the compiler, so fragment loads are LDS, not generic LD
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* sC = reinterpret_cast<double*>(base + (size_t)T::STAGES * T::STAGE_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES + T::C_BYTES);
+  double* sred = reinterpret_cast<double*>(base + (size_t)T::STAGES * T::STAGE_BYTES + T::C_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)T::STAGES * T::STAGE_BYTES + T::C_BYTES +
+                                               (size_t)T::CWARPS * T::RED_WARP * 8);
   uint64_t* empty = full + T::STAGES;
   uint64_t* cbar = empty + T::STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -237,6 +239,34 @@ gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constan
   double* __restrict__ C = g.C + (long long)blockIdx.z * g.c_zstride;
   double* __restrict__ D2 = g.D2;
   const int c0 = frag_row(2 * fc), c1 = frag_row(2 * fc + 1);
+  if constexpr (T::RED) {   // beta = 1: bulk reduce-add of alpha*acc into C (see the persistent kernel)
+    if (g.red_ok && g.beta == 1.0 && g.D2 == nullptr) {
+      const int mw = m0 + wm * T::WM;
+      const int rows = min(T::WM, g.M - mw);
+#pragma unroll
+      for (int j = 0; j < T::NI; ++j) {
+        double* buf = sred + (size_t)warp * T::RED_WARP + (j & 1) * 8 * T::RED_LD;
+        if (lane < 8) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) buf[(h ? c1 : c0) * T::RED_LD + i * 8 + fr] = g.alpha * acc[i][j][h];
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        const int n = n0 + wn * T::WN + j * 8 + lane;
+        if (lane < 8 && rows > 0 && n < g.N) {
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(
+                           C + mw + (long long)n * g.ldc),
+                       "r"(smem_u32(buf + lane * T::RED_LD)), "r"(rows * 8)
+                       : "memory");
+        }
+        if (lane < 8) asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+      if (lane < 8) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+      return;
+    }
+  }
   const bool use_beta = g.beta != 0.0;
   if (cpre) mbar_wait(cbar, 0);
 #pragma unroll

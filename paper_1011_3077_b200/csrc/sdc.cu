@@ -435,6 +435,15 @@ int red_mode() {
   return v;
 }
 
+int side_persist() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("SDC_SIDE_PERSIST");
+    v = e ? atoi(e) : 0;   // 0: one-tile CTAs for side-stream updates (default), 1: persistent
+  }
+  return v;
+}
+
 int persist_mode() {
   static int v = -2;
   if (v == -2) {
@@ -467,6 +476,15 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
     }
     if (v == 4 && !cok) v = 0;
     const int pm = persist_mode();
+    // On the look-ahead side stream the short-K updates use one-tile CTAs: a persistent grid
+    // would hold every SM until the whole update finished, and the critical chain's kernels
+    // (panels, next-block updates, reductions) on the high-priority stream would queue
+    // behind it; one-tile CTAs retire continuously, so the scheduler can hand SMs to them.
+    if (v == 3 && h->on_side && side_persist() == 0) {
+      if (red_mode() && beta == 1.0 && D2 == nullptr && g.red_ok)
+        return launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
+      return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
+    }
     if (pm == 2 || (pm == 1 && v == 3)) {
       switch (v) {
         case 0: return launch_tma_persist<TmaL>(h, A, lda, B, ldb, g, splits);
