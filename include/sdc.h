@@ -28,7 +28,15 @@
  *     SDC_ERR_NOT_SUPPORTED (-102); text of the last error via sdc_last_error();
  *   - numerical outcomes (no split, non-finite) are NOT errors: see sdc_result.status;
  *   - no CPU fallback: without a usable sm_100 device every call fails with -100/-102.
- *   - a handle is not re-entrant: use one handle per concurrent stream.
+ *   - a handle is not re-entrant: use one handle per concurrent stream.  Handles on
+ *     different streams may run concurrently; their results are bit-identical to serial
+ *     runs (tests/test_gpu_concurrency.py);
+ *   - inside a call the handle may fork work from `stream` onto its own streams: a
+ *     high-priority stream for the look-ahead QR chain, and a second factorization
+ *     context for the pencil's left chain or monitor-mode GRURV.  Every fork is joined back
+ *     into `stream` by events before the call's last operation on `stream`, so stream
+ *     ordering for the caller is unchanged.  A fixed-mode step with n <= 4096 is
+ *     additionally replayed as one CUDA graph whose edges carry these forks and joins.
  */
 #ifndef SDC_H
 #define SDC_H
