@@ -104,6 +104,8 @@ struct sdc_handle {
   bool lookahead = true;
   bool on_side = false;                // issuing on the look-ahead side stream
   bool two_chains = false;             // both factorization contexts busy (pencil, Alg. 4)
+  bool xpass_pending = false;          // la_fork / la_B recorded by the previous IRS pass
+  bool xpass_on = true;                // cross-pass look-ahead in the fixed-mode pass loop
   int side_reserve = 0;                // SMs the side stream's persistent GEMMs leave free
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
@@ -123,6 +125,7 @@ struct sdc_handle {
     unsigned long long bar_count = 0;
     unsigned ll_epoch = 0;
     int gemm_force = -1;
+    bool xpass_pending = false;
   } alt;
   int gemm_force = -1;   // debug: force a GEMM variant in this context
   bool alt_ready = false, pipeline = true;
@@ -195,6 +198,7 @@ void swap_ctx(sdc_handle* h) {
   std::swap(h->bar, a.bar); std::swap(h->bar_count, a.bar_count); std::swap(h->ll_epoch, a.ll_epoch);
   std::swap(h->C, a.C); std::swap(h->G1, a.G1); std::swap(h->G2, a.G2); std::swap(h->G3, a.G3);
   std::swap(h->gemm_force, a.gemm_force);
+  std::swap(h->xpass_pending, a.xpass_pending);
 }
 struct AltScope {   // issue on the second context for the scope's lifetime
   sdc_handle* h;
@@ -745,6 +749,10 @@ int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, 
   return rc1;
 }
 
+inline bool lookahead_qr(const sdc_handle* h, int n) {
+  return h->lookahead && h->st_hi && h->nbo > NB && n > 2 * h->nbo;
+}
+
 // panels + inner WY updates + T_O of the outer block at I0 (columns I0..I0+nbo-1 only)
 int factor_block(sdc_handle* h, double* A, long long lda, int m, int n, int I0, int nbo, const Fac& f) {
   for (int i0 = I0; i0 < I0 + nbo; i0 += NB) {
@@ -786,10 +794,15 @@ struct LaScope {   // restores the caller's stream and the primary workspace on 
 
 int blocked_qr_lookahead(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
   LaScope la(h);
-  SDC_CK(cudaEventRecord(h->la_fork, la.side));
+  bool pendingB = false;
+  if (h->xpass_pending) {   // fork point and pending bulk columns left by the previous IRS pass
+    h->xpass_pending = false;
+    pendingB = true;
+  } else {
+    SDC_CK(cudaEventRecord(h->la_fork, la.side));
+  }
   SDC_CK(cudaStreamWaitEvent(h->st_hi, h->la_fork, 0));
   la.use_side(false);
-  bool pendingB = false;
   for (int I0 = 0; I0 < n; I0 += h->nbo) {
     const int nbo = std::min(h->nbo, n - I0);
     SDC_TRY(factor_block(h, A, lda, m, n, I0, nbo, f));
@@ -817,8 +830,8 @@ int blocked_qr_lookahead(sdc_handle* h, double* A, long long lda, int m, int n, 
 // nbo-wide outer blocks (inner WY updates restricted to the block), then one rank-nbo
 // trailing update per outer block.  Factors into f, T blocks into h->Tb / h->Tob.
 int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
-  if (h->lookahead && h->st_hi && h->nbo > NB && n > 2 * h->nbo)
-    return blocked_qr_lookahead(h, A, lda, m, n, f);
+  if (lookahead_qr(h, n)) return blocked_qr_lookahead(h, A, lda, m, n, f);
+  h->xpass_pending = false;
   for (int I0 = 0; I0 < n; I0 += h->nbo) {
     const int nbo = std::min(h->nbo, n - I0);
     for (int i0 = I0; i0 < I0 + nbo; i0 += NB) {
@@ -896,7 +909,7 @@ Fac fac_square(sdc_handle* h, int n) { return Fac{h->Y, (long long)n, h->Yt, (lo
 // ---------------------------------------------------------------------------------------
 int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double* Bj,
              long long ldb, double* An, long long ldan, double* Bn, long long ldbn, double* S,
-             int rtest_slot, double* Rout, long long ldr) {
+             int rtest_slot, double* Rout, long long ldr, bool xpass = false) {
   const long long m = 2LL * n;
   const Fac f = fac_stack(h, n);
   SDC_TRY(blocked_qr(h, S, m, (int)m, n, f));
@@ -920,16 +933,33 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
   k_set_zero_identity<<<ew_grid(m * n), 256, 0, h->st>>>(h->C, m, n);
   SDC_LAUNCHED(h);
   SDC_TRY(apply_q(h, (int)m, n, f, h->C, m, n));
-  // A_{j+1} = Q12^T A_j (-> next stack lower half, negated); B_{j+1} = Q22^T B_j (upper)
-  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C, m, Aj, lda, 0.0, An, ldan, S + n, m, -1.0));
-  if (Bj != nullptr && Bj == h->b_ident) {   // B_j = rho I (first RNEP pass): B_{j+1} = rho Q22^T
+  // A_{j+1} = Q12^T A_j (-> next stack lower half, negated); B_{j+1} = Q22^T B_j (upper).
+  // Cross-pass look-ahead (xpass: the next operation of this context is pass j+1's QR):
+  // the first nbo columns of the next stack are formed first, the fork point of pass j+1's
+  // look-ahead QR is recorded there, and the remaining columns follow as that QR's pending
+  // "bulk update" -- so pass j+1's first block of panels overlaps this pass's products.
+  const bool xp = xpass && lookahead_qr(h, n);
+  const int w = xp ? h->nbo : n;
+  const bool bid = Bj != nullptr && Bj == h->b_ident;   // B_j = rho I (first RNEP pass)
+  if (bid) {                                            // B_{j+1} = rho Q22^T (all columns)
     h->b_ident = nullptr;
     dim3 grid(cdiv(n, 32), cdiv(n, 32));
     k_transpose_scale2<<<grid, dim3(32, 8), 0, h->st>>>(Bn, ldbn, S, m, h->C + n, m, n, h->b_ident_rho);
     SDC_LAUNCHED(h);
-    return 0;
   }
-  SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->C + n, m, Bj, ldb, 0.0, Bn, ldbn, S, m, 1.0));
+  for (int part = 0; part < (xp ? 2 : 1); ++part) {
+    const int c0 = part == 0 ? 0 : w, nc = part == 0 ? w : n - w;
+    SDC_TRY(gemm_tn(h, n, nc, n, 1.0, h->C, m, Aj + (long long)c0 * lda, lda, 0.0, An + (long long)c0 * ldan,
+                    ldan, S + n + (long long)c0 * m, m, -1.0));
+    if (!bid)
+      SDC_TRY(gemm_tn(h, n, nc, n, 1.0, h->C + n, m, Bj + (long long)c0 * ldb, ldb, 0.0,
+                      Bn + (long long)c0 * ldbn, ldbn, S + (long long)c0 * m, m, 1.0));
+    if (xp && part == 0) SDC_CK(cudaEventRecord(h->la_fork, h->st));
+  }
+  if (xp) {
+    SDC_CK(cudaEventRecord(h->la_B, h->st));
+    h->xpass_pending = true;
+  }
   return 0;
 }
 
@@ -1050,6 +1080,7 @@ int reset_sync(sdc_handle* h) {
   SDC_CK(cudaMemsetAsync(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
   h->bar_count = 0;
   h->ll_epoch = 0;
+  h->xpass_pending = h->alt.xpass_pending = false;
   if (h->alt_ready) {   // (on the caller's stream: ordered before any fork to the context)
     SDC_CK(cudaMemsetAsync(h->alt.bar, 0, 64, h->st));
     SDC_CK(cudaMemsetAsync(h->alt.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
@@ -1246,13 +1277,15 @@ int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const do
     TwoChains(sdc_handle* h_, bool on) : h(h_) { h->two_chains = on; }
     ~TwoChains() { h->two_chains = false; }
   } tc(h, two);
+  const bool xpass = h->xpass_on;
   for (int j = 0; j < max_iters; ++j) {
+    const bool more = xpass && j + 1 < max_iters;
     SDC_TRY(irs_pass(h, n, h->A[cur], ld, h->B[cur], ld, h->A[cur ^ 1], ld, h->B[cur ^ 1], ld, h->S, j,
-                     nullptr, 0));
+                     nullptr, 0, more));
     if (two) {
       AltScope as(h);
       SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
-                       h->SL, -1, nullptr, 0));
+                       h->SL, -1, nullptr, 0, more));
     } else if (pencil && !h->ql_orth) {
       SDC_TRY(irs_pass(h, n, h->AL[cur], ld, h->BL[cur], ld, h->AL[cur ^ 1], ld, h->BL[cur ^ 1], ld,
                        h->SL, -1, nullptr, 0));
@@ -1434,6 +1467,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
   if (const char* e = getenv("SDC_LOOKAHEAD")) h->lookahead = atoi(e) != 0;
   if (const char* e = getenv("SDC_SIDE_RESERVE")) h->side_reserve = std::max(0, atoi(e));
+  if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
   if (const char* e = getenv("SDC_MAIN_GEMM")) h->gemm_force = atoi(e);
   if (const char* e = getenv("SDC_ALT_GEMM")) h->alt.gemm_force = atoi(e);

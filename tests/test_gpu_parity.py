@@ -288,12 +288,13 @@ def test_outer_block_widths_parity(orc, sdc, nbo):
     assert info.k == p.expected_k
 
 
-@pytest.mark.parametrize("la", [0, 1])
-def test_lookahead_schedule_parity(orc, sdc, la):
+@pytest.mark.parametrize("la,xp", [(0, 0), (1, 0), (1, 1)])
+def test_lookahead_schedule_parity(orc, sdc, la, xp):
     # look-ahead QR (panels on a high-priority stream, bulk trailing updates overlapped on
-    # the caller's stream) and the serial order give the oracle's invariants at a ragged n
-    # with 4 outer blocks; the R of a 2n x n QR stays the unique diag >= 0 factor
-    h = _handle_with_env(sdc, 900, SDC_LOOKAHEAD=la)
+    # the caller's stream), with and without the cross-pass overlap (pass j+1's first panels
+    # next to pass j's products), and the serial order give the oracle's invariants at a
+    # ragged n with 4 outer blocks; the R of a 2n x n QR stays the unique diag >= 0 factor
+    h = _handle_with_env(sdc, 900, SDC_LOOKAHEAD=la, SDC_XPASS=xp)
     p = inputs.make_config(2, n=900)
     Q, _, Ah, info, o = run_both(orc, h, p)
     assert_parity(o, Q, info, p.A, p.n, Ah)
