@@ -105,7 +105,9 @@ struct sdc_handle {
   bool on_side = false;                // issuing on the look-ahead side stream
   bool two_chains = false;             // both factorization contexts busy (pencil, Alg. 4)
   bool xpass_pending = false;          // la_fork / la_B recorded by the previous IRS pass
-  bool xpass_on = true;                // cross-pass look-ahead in the fixed-mode pass loop
+  bool xpass_on = false;               // cross-pass look-ahead in the fixed-mode pass loop
+                                       // (SDC_XPASS=1; measured no gain: the first panels'
+                                       // cluster waits for the products' CTAs to drain)
   int side_reserve = 0;                // SMs the side stream's persistent GEMMs leave free
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
