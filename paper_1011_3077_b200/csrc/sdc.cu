@@ -130,7 +130,7 @@ struct sdc_handle {
     bool xpass_pending = false;
   } alt;
   int gemm_force = -1;   // debug: force a GEMM variant in this context
-  bool alt_ready = false, pipeline = true;
+  bool alt_ready = false, pipeline = true, alt_fail_hook = false;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;   // cross-context dependencies
   // CUDA graph of the FIXED-mode step (replayed while the call signature is unchanged)
   struct GraphKey {
@@ -1098,6 +1098,7 @@ int ensure_alt(sdc_handle* h) {
   auto& a = h->alt;
   const size_t n = (size_t)h->n_max, nn = n * n;
   int rc = 0;
+  const size_t first_alloc = h->allocs.size();
 #define ALLOC(p, e) \
   if (!rc) rc = dalloc(h, &(p), (e))
   ALLOC(a.Y, 2 * nn);
@@ -1121,6 +1122,18 @@ int ensure_alt(sdc_handle* h) {
     ALLOC(a.Zb2, (size_t)h->nbo * (n + 64));
   }
 #undef ALLOC
+  if (!rc && h->alt_fail_hook) rc = SDC_ERR_NOMEM;   // test hook (SDC_ALT_FAIL_ALLOC): the fallback
+  if (rc == SDC_ERR_NOMEM) {
+    // not enough HBM for a second context next to the handle's workspace: release what was
+    // taken and run every chain on the single context (same results, no overlap)
+    for (size_t i = first_alloc; i < h->allocs.size(); ++i) cudaFree(h->allocs[i]);
+    h->allocs.resize(first_alloc);
+    cudaGetLastError();
+    a = sdc_handle::Ctx{};
+    h->pipeline = false;
+    g_err[0] = 0;
+    return 0;
+  }
   if (rc) return rc;
   void* q = nullptr;
   SDC_CK(cudaMalloc(&q, 64));
@@ -1471,6 +1484,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_SIDE_RESERVE")) h->side_reserve = std::max(0, atoi(e));
   if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
+  if (getenv("SDC_ALT_FAIL_ALLOC")) h->alt_fail_hook = true;
   if (const char* e = getenv("SDC_MAIN_GEMM")) h->gemm_force = atoi(e);
   if (const char* e = getenv("SDC_ALT_GEMM")) h->alt.gemm_force = atoi(e);
   if (!rc && h->lookahead) {

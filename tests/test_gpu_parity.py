@@ -357,6 +357,21 @@ def test_panel_variants_r_unique(orc, sdc, rows, m, n):
     assert np.linalg.norm(host(q) @ host(r) - s) <= 64 * n * EPS * np.linalg.norm(s)
 
 
+def test_second_context_alloc_failure_falls_back(sdc):
+    # when the second context does not fit next to the handle's workspace (simulated), the
+    # pencil and monitor-mode paths run on the single context with bit-identical results
+    p = inputs.make_config(4, n=300)
+    outs = []
+    for env in ({"SDC_PIPELINE": 0}, {"SDC_ALT_FAIL_ALLOC": 1}):
+        h = _handle_with_env(sdc, 300, pencil=True, **env)
+        Q, QL, Ah, info = h.split(dev(p.A), dev(p.B), dev(p.V), dev(p.VL), max_iters=12, want_ahat=True)
+        Q2, _, _, info2 = h.split(dev(p.A), None, dev(p.V), max_iters=12, tol=1e-13, stop="e21")
+        outs.append((Q, QL, info, Q2, info2))
+    (a, b, i, c, j), (a2, b2, i2, c2, j2) = outs
+    assert torch.equal(a, a2) and torch.equal(b, b2) and torch.equal(c, c2)
+    assert (i.k, i.r, i.metric) == (i2.k, i2.r, i2.metric) and (j.k, j.iters) == (j2.k, j2.iters)
+
+
 def test_blocked_qr_two_level_r_unique(orc, sdc):
     # R of the two-level QR equals the oracle's (unique with diag >= 0) at 2n x n, n = 700
     h = _handle_with_env(sdc, 700, SDC_NBO=256)
