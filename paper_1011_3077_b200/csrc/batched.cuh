@@ -375,11 +375,14 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* 
     // (B) reflector (dlarfg, Q7), identical in every thread
     const double alpha = P[k + k * ldp], sigma = g[k];
     double tk = 0.0, scale = 0.0, bk = alpha;
-    if (sigma != 0.0) {
-      const double nrm = sqrt(fma(alpha, alpha, sigma));
+    if (sigma != 0.0) {   // one rsqrt + one reciprocal (the panel kernel's formulas)
+      const double qq = fma(alpha, alpha, sigma);
+      const double rn = rsqrt(qq);
+      const double nrm = qq * rn, aa = fabs(alpha);
       bk = alpha < 0.0 ? nrm : -nrm;
-      tk = (bk - alpha) / bk;
-      scale = 1.0 / (alpha - bk);
+      tk = fma(aa, rn, 1.0);                       // (beta - alpha) / beta
+      const double sa = __drcp_rn(aa + nrm);       // 1 / (alpha - beta) = sign(alpha) / (|alpha| + nrm)
+      scale = alpha < 0.0 ? -sa : sa;
     }
     for (int j = k + 1 + warp; j < n; j += BQ_THREADS / 32) {   // columns j > k
       const double w = tk * fma(scale, g[j], P[k + j * ldp]);
