@@ -364,12 +364,29 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* 
   for (int e = tid; e < np * np; e += BQ_THREADS) T[e] = 0.0;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    // (A) g_j = sum_{r > k} x_k(r) P(r, j), every column j (j < k: Gram entries for T)
-    for (int j = warp; j < n; j += BQ_THREADS / 32) {
-      double s = 0.0;
-      for (int r = k + 1 + lane; r < m; r += 32) s = fma(P[r + k * ldp], P[r + j * ldp], s);
-      s = warp_sum(s);
-      if (lane == 0) g[j] = s;
+    // (A) g_j = sum_{r > k} x_k(r) P(r, j), every column j (j < k: Gram entries for T).
+    // A warp owns 4 consecutive columns; the 4 lane sums are reduced by recursive halving
+    // (xor 16 and 8 exchange half of the columns, xor 4, 2, 1 finish): 6 shuffles instead
+    // of 4 full butterflies (20), fixed order per column.
+    for (int jb = warp * 4; jb < n; jb += BQ_THREADS / 8) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int r = k + 1 + lane; r < m; r += 32) {
+        const double x = P[r + k * ldp];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (jb + c < n) s[c] = fma(x, P[r + (jb + c) * ldp], s[c]);
+      }
+      const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+      double k0 = h16 ? s[2] : s[0], k1 = h16 ? s[3] : s[1];
+      k0 += __shfl_xor_sync(0xffffffffu, h16 ? s[0] : s[2], 16);
+      k1 += __shfl_xor_sync(0xffffffffu, h16 ? s[1] : s[3], 16);
+      double v = h8 ? k1 : k0;
+      v += __shfl_xor_sync(0xffffffffu, h8 ? k0 : k1, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      const int c = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+      if ((lane & 7) == 0 && jb + c < n) g[jb + c] = v;
     }
     __syncthreads();
     // (B) reflector (dlarfg, Q7), identical in every thread
