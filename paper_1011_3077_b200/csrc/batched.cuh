@@ -358,10 +358,10 @@ SDC_DEV void bq_mma(int P_, int Q_, int K_, FA fa, FB fb, FO fo) {
 // unscaled Householder QR of the m x n P (ld ldp) with compact-WY T (NP x NP, ld np, upper):
 // on exit P holds x_k below the diagonal (v_k = sc[k] x_k, unit diagonal implied), R above,
 // beta[k] = R(k, k); I - Y T Y^T = H_0 ... H_{n-1}.  Two CTA barriers per column.
-SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* sc, double* tau,
-                   double* beta, double* g) {
+SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, int tld, double* sc,
+                   double* beta, double* g, double* drow) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < np * np; e += BQ_THREADS) T[e] = 0.0;
+  for (int e = tid; e < np * tld; e += BQ_THREADS) T[e] = 0.0;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
     // (A) g_j = sum_{r > k} x_k(r) P(r, j), every column j (j < k: Gram entries for T).
@@ -386,7 +386,10 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* 
       v += __shfl_xor_sync(0xffffffffu, v, 2);
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       const int c = (h16 ? 2 : 0) + (h8 ? 1 : 0);
-      if ((lane & 7) == 0 && jb + c < n) g[jb + c] = v;
+      if ((lane & 7) == 0 && jb + c < n) {
+        g[jb + c] = v;
+        drow[jb + c] = P[k + (jb + c) * ldp];   // x_j(k): row k, read by the T column below
+      }
     }
     __syncthreads();
     // (B) reflector (dlarfg, Q7), identical in every thread
@@ -413,14 +416,13 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, double* 
       const int i = tid >> 2, q = tid & 3;
       double acc = 0.0;
       if (i < k)
-        for (int l = i + q; l < k; l += 4) acc = fma(T[i + l * np], sc[l] * fma(scale, g[l], P[k + l * ldp]), acc);
+        for (int l = i + q; l < k; l += 4) acc = fma(T[i + l * tld], sc[l] * fma(scale, g[l], drow[l]), acc);
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (i < k && q == 0) T[i + k * np] = -tk * acc;
+      if (i < k && q == 0) T[i + k * tld] = -tk * acc;
       if (tid == 0) {
-        T[k + k * np] = tk;
+        T[k + k * tld] = tk;
         sc[k] = scale;
-        tau[k] = tk;
         beta[k] = bk;
       }
     }
@@ -435,12 +437,12 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   double* Aj = smq;                 // np x np
   double* Bj = Aj + NN;
   double* P = Bj + NN;              // 2np x np: stack / factored matrices
-  double* T = P + 2 * NN;           // np x np
-  double* Z = T + NN;
+  double* T = P + 2 * NN;           // np x np, ld tld = np + 1 (odd: conflict-free T column loop)
+  const int tld = np + 1;
+  double* Z = T + NN + np;
   double* W = Z + NN;
   double* sc = W + NN;              // np
-  double* tau = sc + np;
-  double* beta = tau + np;
+  double* beta = sc + np;
   double* g = beta + np;            // np
   double* msel = g + np;            // np
   double* red = msel + np;          // 2 * BAT_WARPS + 16
@@ -483,9 +485,9 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
       P[e] = v;
     }
     __syncthreads();
-    bq_qr(m, n, np, P, ldp, T, sc, tau, beta, g);
+    bq_qr(m, n, np, P, ldp, T, tld, sc, beta, g, msel);
     // Z = T Y2^T
-    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * np]; },
+    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * tld]; },
            [&](int k, int j) { return Yv(n + j, k, m); },
            [&](int i, int j, double v) { Z[i + j * np] = v; });
     // W = Y1^T A_j ;  A_{j+1} = -Z^T W
@@ -509,14 +511,14 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   bq_mma(np, np, np, [&](int i, int k) { return Aj[i + k * np]; },
          [&](int k, int j) { return (k < n && j < n) ? V0[j + (long long)k * a.ldv] : 0.0; },
          [&](int i, int j, double v) { P[i + j * ldp] = v; });
-  bq_qr(n, n, np, P, ldp, T, sc, tau, beta, g);                   // X = U R_2
+  bq_qr(n, n, np, P, ldp, T, tld, sc, beta, g, msel);                   // X = U R_2
   for (int e = tid; e < NN; e += BQ_THREADS) Aj[e] += Bj[e];       // S = A_p + B_p
   __syncthreads();
   // U^T S = S - Y T^T (Y^T S)
   bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
          [&](int k, int j) { return Aj[k + j * np]; },
          [&](int i, int j, double v) { W[i + j * np] = v; });
-  bq_mma(np, np, np, [&](int i, int k) { return T[k + i * np]; },
+  bq_mma(np, np, np, [&](int i, int k) { return T[k + i * tld]; },
          [&](int k, int j) { return W[k + j * np]; },
          [&](int i, int j, double v) { Z[i + j * np] = v; });
   bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
@@ -531,9 +533,9 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
     P[e] = (i < n && j < n) ? Aj[(n - 1 - j) + i * np] : 0.0;
   }
   __syncthreads();
-  bq_qr(n, n, np, P, ldp, T, sc, tau, beta, g);
+  bq_qr(n, n, np, P, ldp, T, tld, sc, beta, g, msel);
   // Q_qr = I - Y (T Y^T):  W = T Y^T, Z = I - Y W
-  bq_mma(np, np, np, [&](int i, int k) { return T[i + k * np]; },
+  bq_mma(np, np, np, [&](int i, int k) { return T[i + k * tld]; },
          [&](int k, int j) { return Yv(j, k, n); },
          [&](int i, int j, double v) { W[i + j * np] = v; });
   bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
