@@ -433,15 +433,16 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, int tld,
 __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArgs a) {
   extern __shared__ __align__(16) double smq[];
   const int n = a.n, m = 2 * n, b = blockIdx.x, tid = threadIdx.x;
-  const int np = (n + 15) & ~15, NN = np * np, ldp = 2 * np;
-  double* Aj = smq;                 // np x np
-  double* Bj = Aj + NN;
-  double* P = Bj + NN;              // 2np x np: stack / factored matrices
-  double* T = P + 2 * NN;           // np x np, ld tld = np + 1 (odd: conflict-free T column loop)
-  const int tld = np + 1;
-  double* Z = T + NN + np;
-  double* W = Z + NN;
-  double* sc = W + NN;              // np
+  // leading dimensions = 4 (mod 16) doubles: the DMMA fragment loads (8 rows x 4 k of one
+  // operand per instruction) and the T column loop hit 16 distinct bank pairs per half-warp
+  const int np = (n + 15) & ~15, ld = np + 4, NL = ld * np, ldp = 2 * np + 4;
+  double* Aj = smq;                 // np x np (ld)
+  double* Bj = Aj + NL;
+  double* P = Bj + NL;              // 2np x np (ldp): stack / factored matrices
+  double* T = P + (size_t)ldp * np; // np x np (ld); W aliases T (T is dead whenever W is live)
+  double* W = T;
+  double* Z = T + NL;
+  double* sc = Z + NL;              // np
   double* beta = sc + np;
   double* g = beta + np;            // np
   double* msel = g + np;            // np
@@ -449,21 +450,21 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   const double* A0 = a.A + (long long)b * a.sa;
   const double* V0 = a.V + (long long)b * a.sv;
 
-  for (int e = tid; e < NN; e += BQ_THREADS) {
+  for (int e = tid; e < np * np; e += BQ_THREADS) {
     const int i = e % np, j = e / np;
     const bool in = i < n && j < n;
-    Aj[e] = in ? A0[i + (long long)j * a.lda] : 0.0;
-    Bj[e] = (in && i == j) ? 1.0 : 0.0;
+    Aj[i + j * ld] = in ? A0[i + (long long)j * a.lda] : 0.0;
+    Bj[i + j * ld] = (in && i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
   double nA = 0.0, fA;
   {
     double f = 0.0;
-    for (int e = tid; e < NN; e += BQ_THREADS) f += Aj[e] * Aj[e];
+    for (int e = tid; e < np * np; e += BQ_THREADS) { const double v = Aj[e % np + (e / np) * ld]; f += v * v; }
     fA = sqrt(bat_sum(f, red));
     if (tid < n) {
       double c = 0.0;
-      for (int i = 0; i < n; ++i) c += fabs(Aj[i + tid * np]);
+      for (int i = 0; i < n; ++i) c += fabs(Aj[i + tid * ld]);
       msel[tid] = c;
     }
     __syncthreads();
@@ -478,94 +479,97 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
 
   // ---- IRS passes (Alg. 3) -----------------------------------------------------------
   for (int pass = 0; pass < a.passes; ++pass) {
-    for (int e = tid; e < 2 * NN; e += BQ_THREADS) {   // P = [B_j; -A_j] (rows >= 2n zero)
+    for (int e = tid; e < ldp * np; e += BQ_THREADS) {   // P = [B_j; -A_j] (rows >= 2n zero)
       const int i = e % ldp, j = e / ldp;
       double v = 0.0;
-      if (j < n) v = i < n ? Bj[i + j * np] : (i < m ? -Aj[(i - n) + j * np] : 0.0);
+      if (j < n) v = i < n ? Bj[i + j * ld] : (i < m ? -Aj[(i - n) + j * ld] : 0.0);
       P[e] = v;
     }
     __syncthreads();
-    bq_qr(m, n, np, P, ldp, T, tld, sc, beta, g, msel);
-    // Z = T Y2^T
-    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * tld]; },
+    bq_qr(m, n, np, P, ldp, T, ld, sc, beta, g, msel);
+    // Z = T Y2^T  (T dead afterwards: W may overwrite it)
+    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * ld]; },
            [&](int k, int j) { return Yv(n + j, k, m); },
-           [&](int i, int j, double v) { Z[i + j * np] = v; });
+           [&](int i, int j, double v) { Z[i + j * ld] = v; });
     // W = Y1^T A_j ;  A_{j+1} = -Z^T W
     bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
-           [&](int k, int j) { return Aj[k + j * np]; },
-           [&](int i, int j, double v) { W[i + j * np] = v; });
-    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * np]; },
-           [&](int k, int j) { return W[k + j * np]; },
-           [&](int i, int j, double v) { Aj[i + j * np] = -v; });
+           [&](int k, int j) { return Aj[k + j * ld]; },
+           [&](int i, int j, double v) { W[i + j * ld] = v; });
+    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
+           [&](int k, int j) { return W[k + j * ld]; },
+           [&](int i, int j, double v) { Aj[i + j * ld] = -v; });
     // W = Y2^T B_j ;  B_{j+1} = B_j - Z^T W
     bq_mma(np, np, np, [&](int i, int k) { return Yv(n + k, i, m); },
-           [&](int k, int j) { return Bj[k + j * np]; },
-           [&](int i, int j, double v) { W[i + j * np] = v; });
-    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * np]; },
-           [&](int k, int j) { return W[k + j * np]; },
-           [&](int i, int j, double v) { Bj[i + j * np] -= v; });
+           [&](int k, int j) { return Bj[k + j * ld]; },
+           [&](int i, int j, double v) { W[i + j * ld] = v; });
+    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
+           [&](int k, int j) { return W[k + j * ld]; },
+           [&](int i, int j, double v) { Bj[i + j * ld] -= v; });
   }
 
   // ---- GRURV(2, A_p + B_p, A_p; -1, +1) ------------------------------------------------
   // X = A_p V^T into P (ld 2np)
-  bq_mma(np, np, np, [&](int i, int k) { return Aj[i + k * np]; },
+  bq_mma(np, np, np, [&](int i, int k) { return Aj[i + k * ld]; },
          [&](int k, int j) { return (k < n && j < n) ? V0[j + (long long)k * a.ldv] : 0.0; },
          [&](int i, int j, double v) { P[i + j * ldp] = v; });
-  bq_qr(n, n, np, P, ldp, T, tld, sc, beta, g, msel);                   // X = U R_2
-  for (int e = tid; e < NN; e += BQ_THREADS) Aj[e] += Bj[e];       // S = A_p + B_p
-  __syncthreads();
-  // U^T S = S - Y T^T (Y^T S)
-  bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
-         [&](int k, int j) { return Aj[k + j * np]; },
-         [&](int i, int j, double v) { W[i + j * np] = v; });
-  bq_mma(np, np, np, [&](int i, int k) { return T[k + i * tld]; },
-         [&](int k, int j) { return W[k + j * np]; },
-         [&](int i, int j, double v) { Z[i + j * np] = v; });
-  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
-         [&](int k, int j) { return Z[k + j * np]; },
-         [&](int i, int j, double v) {
-           const double s = Aj[i + j * np] - v;
-           Aj[i + j * np] = (i < n && beta[i] < 0.0) ? -s : s;     // U <- U D_U
-         });
-  // M = C^T J into P: M(i, j) = C(n-1-j, i)
-  for (int e = tid; e < 2 * NN; e += BQ_THREADS) {
-    const int i = e % ldp, j = e / ldp;
-    P[e] = (i < n && j < n) ? Aj[(n - 1 - j) + i * np] : 0.0;
+  bq_qr(n, n, np, P, ldp, T, ld, sc, beta, g, msel);                    // X = U R_2
+  for (int e = tid; e < np * np; e += BQ_THREADS) {                   // S = A_p + B_p
+    const int i = e % np, j = e / np;
+    Aj[i + j * ld] += Bj[i + j * ld];
   }
   __syncthreads();
-  bq_qr(n, n, np, P, ldp, T, tld, sc, beta, g, msel);
-  // Q_qr = I - Y (T Y^T):  W = T Y^T, Z = I - Y W
-  bq_mma(np, np, np, [&](int i, int k) { return T[i + k * tld]; },
-         [&](int k, int j) { return Yv(j, k, n); },
-         [&](int i, int j, double v) { W[i + j * np] = v; });
+  // U^T S = S - (Y T^T)(Y^T S):  Z = Y T^T (last use of T), W = Y^T S, S -= Z W, row signs
   bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
-         [&](int k, int j) { return W[k + j * np]; },
-         [&](int i, int j, double v) { Z[i + j * np] = (i == j && i < n ? 1.0 : 0.0) - v; });
+         [&](int k, int j) { return T[j + k * ld]; },
+         [&](int i, int j, double v) { Z[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
+         [&](int k, int j) { return Aj[k + j * ld]; },
+         [&](int i, int j, double v) { W[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Z[i + k * ld]; },
+         [&](int k, int j) { return W[k + j * ld]; },
+         [&](int i, int j, double v) {
+           const double s = Aj[i + j * ld] - v;
+           Aj[i + j * ld] = (i < n && beta[i] < 0.0) ? -s : s;     // U <- U D_U
+         });
+  // M = C^T J into P: M(i, j) = C(n-1-j, i)
+  for (int e = tid; e < ldp * np; e += BQ_THREADS) {
+    const int i = e % ldp, j = e / ldp;
+    P[e] = (i < n && j < n) ? Aj[(n - 1 - j) + i * ld] : 0.0;
+  }
+  __syncthreads();
+  bq_qr(n, n, np, P, ldp, T, ld, sc, beta, g, msel);
+  // Q_qr = I - (Y T) Y^T:  Z = Y T (last use of T), W = I - Z Y^T
+  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
+         [&](int k, int j) { return T[k + j * ld]; },
+         [&](int i, int j, double v) { Z[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Z[i + k * ld]; },
+         [&](int k, int j) { return Yv(j, k, n); },
+         [&](int i, int j, double v) { W[i + j * ld] = (i == j && i < n ? 1.0 : 0.0) - v; });
   // Q(:, j) = sign(R(jj, jj)) Q_qr(:, jj), jj = n-1-j  -> Bj
-  for (int e = tid; e < NN; e += BQ_THREADS) {
+  for (int e = tid; e < np * np; e += BQ_THREADS) {
     const int i = e % np, j = e / np;
     double v = 0.0;
     if (i < n && j < n) {
       const int jj = n - 1 - j;
-      v = (beta[jj] < 0.0 ? -1.0 : 1.0) * Z[i + jj * np];
+      v = (beta[jj] < 0.0 ? -1.0 : 1.0) * W[i + jj * ld];
     }
-    Bj[e] = v;
+    Bj[i + j * ld] = v;
   }
   __syncthreads();
 
   // ---- similarity Ahat = Q^T A Q (original A), split selection ------------------------------
   bq_mma(np, np, np, [&](int i, int k) { return (i < n && k < n) ? A0[i + (long long)k * a.lda] : 0.0; },
-         [&](int k, int j) { return Bj[k + j * np]; },
-         [&](int i, int j, double v) { W[i + j * np] = v; });
-  bq_mma(np, np, np, [&](int i, int k) { return Bj[k + i * np]; },
-         [&](int k, int j) { return W[k + j * np]; },
-         [&](int i, int j, double v) { Aj[i + j * np] = v; });
-  // suffix column sums: Z[c + r np] = sum_{i >= r} |Ahat(i, c)| for c < r
+         [&](int k, int j) { return Bj[k + j * ld]; },
+         [&](int i, int j, double v) { W[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Bj[k + i * ld]; },
+         [&](int k, int j) { return W[k + j * ld]; },
+         [&](int i, int j, double v) { Aj[i + j * ld] = v; });
+  // suffix column sums: Z[c + r ld] = sum_{i >= r} |Ahat(i, c)| for c < r
   if (tid < n) {
     double s = 0.0;
     for (int r = n - 1; r >= 1; --r) {
-      s += fabs(Aj[r + tid * np]);
-      Z[tid + r * np] = s;
+      s += fabs(Aj[r + tid * ld]);
+      Z[tid + r * ld] = s;
     }
   }
   __syncthreads();
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
     const int r = tid;
     double ma = 0.0;
     for (int c = 0; c < r; ++c) {
-      const double v = Z[c + r * np];
+      const double v = Z[c + r * ld];
       if (v > ma || v != v) ma = v;
     }
     msel[r] = ma / nA;
@@ -589,10 +593,10 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   __syncthreads();
   const int rbest = (int)red[2 * BAT_WARPS];
   double f = 0.0, nf = 0.0;
-  for (int e = tid; e < NN; e += BQ_THREADS) {
+  for (int e = tid; e < np * np; e += BQ_THREADS) {
     const int i = e % np, j = e / np;
     if (i >= n || j >= n) continue;
-    const double v = Aj[e];
+    const double v = Aj[i + j * ld];
     if (i >= rbest && j < rbest) f += v * v;
     if (!(fabs(v) <= 1.79e308)) nf = 1.0;
   }
@@ -601,7 +605,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   double* Qo = a.Q + (long long)b * a.sq;
   for (int e = tid; e < n * n; e += BQ_THREADS) {
     const int i = e % n, j = e / n;
-    Qo[i + (long long)j * a.ldq] = Bj[i + j * np];
+    Qo[i + (long long)j * a.ldq] = Bj[i + j * ld];
   }
   if (tid == 0) {
     a.out[4 * b + 0] = rbest;
@@ -612,8 +616,8 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
 }
 
 inline size_t bq_smem_bytes(int n) {
-  const size_t np = (size_t)((n + 15) & ~15);
-  return sizeof(double) * (7 * np * np + 5 * np + 2 * BAT_WARPS + 16);
+  const size_t np = (size_t)((n + 15) & ~15), ld = np + 4, ldp = 2 * np + 4;
+  return sizeof(double) * (4 * ld * np + ldp * np + 4 * np + 2 * BAT_WARPS + 16);
 }
 
 }  // namespace sdc
