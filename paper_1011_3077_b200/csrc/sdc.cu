@@ -753,11 +753,13 @@ int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, 
   return rc1;
 }
 
-// outer block width for an order-n step: 128 up to n = 4096 (shorter inner-update and
-// T-merge chains between panels; measured 3.5% faster at n = 1024, 1% at n = 4096), the
-// full 256 above (rank-256 updates run closer to the DMMA peak at n = 16384)
+// outer block width for an order-n step (measured): 64 up to n = 1024 (single-level
+// blocking: no T merges or nested updates between panels; 6% faster than 256 at n = 1024),
+// 128 up to n = 4096 (1% faster than 256 at n = 4096, 15% faster than 64), the full 256
+// above (rank-256 updates run closer to the DMMA peak at n = 16384)
 inline void choose_nbo(sdc_handle* h, int n) {
-  h->nbo = (h->nbo_fixed || n > 4096) ? h->nbo_max : std::min(h->nbo_max, 128);
+  if (h->nbo_fixed || n > 4096) h->nbo = h->nbo_max;
+  else h->nbo = std::min(h->nbo_max, n <= 1024 ? 64 : 128);
 }
 
 inline bool lookahead_qr(const sdc_handle* h, int n) {
