@@ -755,10 +755,13 @@ int wy_apply_outer(sdc_handle* h, int trans, int I0, int nbo, int m, int ncols, 
 
 // outer block width for an order-n step (measured): 64 up to n = 1024 (single-level
 // blocking: no T merges or nested updates between panels; 6% faster than 256 at n = 1024),
-// 128 up to n = 4096 (1% faster than 256 at n = 4096, 15% faster than 64), the full 256
-// above (rank-256 updates run closer to the DMMA peak at n = 16384)
-inline void choose_nbo(sdc_handle* h, int n) {
-  if (h->nbo_fixed || n > 4096) h->nbo = h->nbo_max;
+// 128 up to n = 4096 / 8192 (1-2% faster than 256, 15% faster than 64 at n = 4096), the
+// full 256 above (rank-256 updates run closer to the DMMA peak at n = 16384).
+// Two concurrent chains (Alg. 4 pencils) keep 256 above n = 4096 (1.4% faster at n = 8192
+// than 128); a single chain uses 128 up to n = 8192 (2% faster than 256 there).
+inline void choose_nbo(sdc_handle* h, int n, bool two_chains = false) {
+  const int lim128 = two_chains ? 4096 : 8192;
+  if (h->nbo_fixed || n > lim128) h->nbo = h->nbo_max;
   else h->nbo = std::min(h->nbo_max, n <= 1024 ? 64 : 128);
 }
 
@@ -1840,7 +1843,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   if (hist_cap < 0 || (hist_cap > 0 && !hist)) { set_err("bad hist"); return -23; }
   if (!res) { set_err("res is NULL"); return -24; }
   if (stop_mode == SDC_STOP_E21 || (pencil && !h->ql_orth)) SDC_TRY(ensure_alt(h));
-  choose_nbo(h, n);
+  choose_nbo(h, n, pencil && !h->ql_orth && h->alt_ready);
   h->st = static_cast<cudaStream_t>(stream);
   h->cur_V = V; h->cur_ldv = ldv; h->cur_VL = VL; h->cur_ldvl = ldvl;
   const bool pencil_ = pencil;
