@@ -141,11 +141,12 @@ def _random_known(n, seed):
     return S @ T @ np.linalg.inv(S), np.array(lams)
 
 
-@pytest.mark.parametrize("n,seed", [(2, 1), (3, 2), (4, 3), (5, 4), (6, 5), (7, 6), (8, 7), (8, 8)])
+@pytest.mark.parametrize("n,seed", [(2, 0), (3, 2), (4, 0), (5, 4), (6, 5), (7, 6), (8, 7), (8, 8)])
 def test_small_n_eigenvalues_match_charpoly(orc, n, seed):
+    # seeds chosen so every spectrum has eigenvalues on both sides of the circle (a
+    # one-sided spectrum has no split to check); asserted, never skipped
     a, lams = _random_known(n, 600 + seed)
-    if np.all(np.abs(lams) > 1) or np.all(np.abs(lams) < 1):
-        pytest.skip("one-sided spectrum")
+    assert np.any(np.abs(lams) > 1) and np.any(np.abs(lams) < 1)
     res = orc.split(a, V=haar(n, 700 + seed), max_iters=14)
     r = res.r
     assert res.k == int(np.sum(np.abs(lams) < 1))
@@ -272,3 +273,87 @@ def test_pencil_qz_count_and_block_triangular(orc, n, seed):
     l22 = sla.eigvals(ah[r:, r:], bh[r:, r:])
     assert np.all(np.abs(l11) > 1) and np.all(np.abs(l22) < 1)
     assert orth_err(res.Q) <= 1e-13 * n and orth_err(res.QL) <= 1e-13 * n
+
+
+# ---------------------------------------------------------------------------------------
+# R-test ratio, status rule and the Frobenius diagnostic (Alg. 3 line 4;
+# DESIGN.md readings Q2, Q4, Q5) -- pinned against independent computations
+# ---------------------------------------------------------------------------------------
+def _numpy_irs_r(a, b, passes):
+    """R_j (diag >= 0) of passes j = 0..passes-1 by an independent IRS in numpy/LAPACK:
+    full QR of [B_j; -A_j] (numpy.linalg.qr, complete mode), Q12 = Q(0:n, n:2n) multiplies
+    A_j, Q22 = Q(n:2n, n:2n) multiplies B_j."""
+    n = a.shape[0]
+    rs = []
+    for _ in range(passes):
+        q, r = np.linalg.qr(np.vstack([b, -a]), mode="complete")
+        d = np.where(np.diag(r[:n]) < 0, -1.0, 1.0)
+        rs.append(d[:, None] * r[:n])
+        a, b = q[:n, n:].T @ a, q[n:, n:].T @ b
+    return rs
+
+
+def test_rtest_ratio_matches_independent_irs(orc):
+    # hist[:, 2] = ||R_j - R_{j-1}||_1 / ||R_{j-1}||_1 (NaN at j = 0, reading Q5), with the
+    # R_j of an independent numpy IRS; compared where the ratio is far above rounding
+    p = inputs.make_config(1)
+    passes = 8
+    res = orc.split(p.A, V=p.V, max_iters=passes, stop=orc.STOP_FIXED)
+    rs = _numpy_irs_r(p.A, np.eye(p.n), passes)
+    want = [np.linalg.norm(rs[j] - rs[j - 1], 1) / np.linalg.norm(rs[j - 1], 1) for j in range(1, passes)]
+    got = res.hist[1:passes, 2]
+    assert np.isnan(res.hist[0, 2])
+    big = np.array(want) > 1e-6
+    assert big.sum() >= 4
+    assert np.allclose(got[big], np.array(want)[big], rtol=1e-7, atol=0)
+
+
+def test_rtest_stops_at_first_eligible_pass(orc):
+    # A = I, B = 0: R_0 = I (stack [0; -I]), A_1 = Q12^T orthogonal, B_1 = 0, so R_1 = I and the
+    # ratio at j = 1 is exactly 0: the R-test (first eligible at j = 1, reading Q5) stops
+    # with p = j + 1 = 2
+    n = 6
+    res = orc.split(np.eye(n), B=np.zeros((n, n)), V=haar(n, 90), VL=haar(n, 91), max_iters=10,
+                    tol=1e-14, stop=orc.STOP_RTEST)
+    assert res.converged == 1 and res.iters == 2
+    assert res.hist[1, 2] <= 1e-14
+
+
+@pytest.mark.parametrize("theta", [1e-4, 0.3])
+def test_rotation_closed_form_metric_and_status(orc, theta):
+    # A = rotation by theta (both eigenvalues on the unit circle: no split).  Any orthogonal
+    # similarity of a 2x2 rotation is a rotation by +-theta, so at r = 1 (the only split)
+    # |E21| = sin(theta) whatever Q the method returns: metric = sin/(cos + sin) (1-norm,
+    # Q2/Q3) and metric_fro = sin/sqrt(2) (F-norm); the metric is far above the 1e-8
+    # acceptance threshold, so status = NO_SPLIT (reading Q4)
+    c, s = np.cos(theta), np.sin(theta)
+    a = np.array([[c, -s], [s, c]])
+    res = orc.split(a, V=haar(2, 92), max_iters=12)
+    assert res.r == 1 and res.k == 1
+    assert res.metric == pytest.approx(s / (c + s), rel=1e-10)
+    assert res.metric_fro == pytest.approx(s / np.sqrt(2.0), rel=1e-10)
+    assert res.status == orc.STATUS_NO_SPLIT
+
+
+def test_status_threshold_reading_q4(orc):
+    # status 0 iff metric <= 1e-8 (reading Q4): a diagonal pencil splits to rounding (status 0);
+    # a rotation by 1e-6 gives metric ~1e-6 in (1e-8, 1e-3) -> status 1
+    res = orc.split(np.diag([2.0, 0.5]), V=haar(2, 93), max_iters=12)
+    assert res.metric <= 1e-14 and res.status == orc.STATUS_SPLIT
+    t = 1e-6
+    a = np.array([[np.cos(t), -np.sin(t)], [np.sin(t), np.cos(t)]])
+    res = orc.split(a, V=haar(2, 94), max_iters=12)
+    assert 1e-8 < res.metric < 1e-3 and res.status == orc.STATUS_NO_SPLIT
+
+
+def test_metric_fro_is_frobenius_e21(orc):
+    # metric_fro = ||Ahat(r+1:n, 1:r)||_F / ||A||_F at the selected r (reading Q2); Ahat itself
+    # is pinned as Q^T A Q with Q orthogonal; checked at a pass where E21 is not yet tiny
+    p = inputs.make_config(1)
+    res = orc.split(p.A, V=p.V, max_iters=3)
+    r = res.r
+    want = np.linalg.norm(res.Ahat[r:, :r]) / np.linalg.norm(p.A)
+    assert want > 1e-6
+    assert res.metric_fro == pytest.approx(want, rel=1e-12)
+    want1 = np.abs(res.Ahat[r:, :r]).sum(axis=0).max() / np.abs(p.A).sum(axis=0).max()
+    assert res.metric == pytest.approx(want1, rel=1e-12)
