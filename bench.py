@@ -123,17 +123,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # CPU oracle: a bounded sample, extrapolated by the flop model
 # ---------------------------------------------------------------------------------------
-def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 1536):
+def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 1536, cfg: int = 5,
+                  monitor: bool = False, ql_orth: bool = False):
     """Time the plain oracle (as it stands) on a same-recipe sample at n_sample: two IRS
     passes (median) and one full split with a single pass; GRURV + similarity + selection
-    = split(1 pass) - pass.  Returns the extrapolated seconds of one full step at n_target
-    (each part scaled by n^3, the flop model's order), threads, description, CPU seconds."""
+    = split(1 pass) - IRS pass(es).  A step is passes x IRS (x2 for Alg. 4's left chain) +
+    one GRURV/similarity/selection, or one after EVERY pass in monitor mode (config 3,
+    PAPER.md:597).  Returns the extrapolated seconds of one full step at n_target (each part
+    scaled by n^3, the flop model's order), threads, description, CPU seconds."""
     import oracle
     from paper_1011_3077_b200 import inputs
     oracle.build()
     threads = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    p = inputs.make_config(4 if pencil else 5, n=n_sample)
+    rc = {9: 4, 6: 5, 7: 5, 8: 5, 10: 1}.get(cfg, cfg)
+    p = inputs.make_config(rc, n=n_sample)
+    if rc == 1 or rc == 3:   # same recipe at n_sample
+        p = inputs.make_config(3, n=n_sample)
     b0 = p.B if pencil else np.eye(n_sample)
     oracle.irs_pass(p.A[:64, :64], b0[:64, :64])          # warm the thread pool
     t_spent = time.perf_counter()
@@ -142,16 +148,19 @@ def oracle_sample(n_target: int, passes: int, pencil: bool, n_sample: int = 1536
         t0 = time.perf_counter()
         oracle.irs_pass(p.A, b0)
         tp.append(time.perf_counter() - t0)
-    per_pass = statistics.median(tp) * (2 if pencil else 1)
+    chains = 2 if (pencil and not ql_orth) else 1
+    per_pass = statistics.median(tp) * chains
     t0 = time.perf_counter()
-    oracle.split(p.A, p.B, p.V, p.VL, max_iters=1)
+    oracle.split(p.A, p.B if pencil else None, p.V, None if ql_orth else p.VL, max_iters=1,
+                 flags=oracle.FLAG_QL_ORTH if ql_orth else 0)
     t1 = time.perf_counter() - t0
     rest = max(t1 - per_pass, 1e-9)
     scale = (n_target / n_sample) ** 3
-    total = (passes * per_pass + rest) * scale
-    sample = (f"oracle at n={n_sample} (same recipe): {per_pass:.2f} s per IRS pass (median of 2), "
-              f"{rest:.2f} s GRURV+similarity+select; extrapolated by n^3 to n={n_target}, "
-              f"{passes} passes")
+    total = (passes * per_pass + (passes if monitor else 1) * rest) * scale
+    sample = (f"oracle at n={n_sample} (same recipe): {per_pass:.2f} s per IRS pass"
+              f"{' (both chains)' if chains == 2 else ''} (median of 2), {rest:.2f} s "
+              f"GRURV+similarity+select{' per pass (monitor mode)' if monitor else ''}; "
+              f"extrapolated by n^3 to n={n_target}, {passes} passes")
     return total, threads, sample, time.perf_counter() - t_spent
 
 
@@ -162,7 +171,8 @@ def run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg=5):
     threads = len(os.sched_getaffinity(0))
     sample = ""
     for i in range(args.warmup + args.steps):
-        total, threads, sample, _ = oracle_sample(n, passes, pencil, n_sample=args.ref_n)
+        total, threads, sample, _ = oracle_sample(n, passes, pencil, n_sample=args.ref_n, cfg=cfg,
+                                                  monitor=(cfg == 3), ql_orth=(cfg == 9))
         if i >= args.warmup:
             steps.append(total)
     t = statistics.median(steps)
@@ -172,7 +182,7 @@ def run_reference(args, cfg_name, n, passes, pencil, rank, world, cfg=5):
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": run_config(cfg_name, n, passes, "e21" if cfg == 3 else "fixed", 1),
-            "tflops_effective": flop_model(n, passes, pencil) / t / 1e12,
+            "tflops_effective": flop_model(n, passes, pencil and cfg != 9, monitor=(cfg == 3)) / t / 1e12,
             "cpu_baseline": {"value": val, "unit": "split steps/s", "cores": threads,
                              "kind": "oracle", "sample": sample + " (extrapolated)"},
             "e2e": {"value": val, "unit": "split steps/s", "h2d_bytes_per_step": 0,
@@ -462,7 +472,7 @@ def run_batched(args, rank, world, local):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg10: {batch} independent RNEP steps per GPU, n={n}, A ~ N(0, 2/n), "
-                                   f"Haar V, {passes} passes, one CTA per problem (k_split_batched)",
+                                   f"Haar V, {passes} passes, one CTA per problem (k_split_batched_wy)",
                        "n": n, "batch_per_gpu": batch, "passes": passes,
                        "parallelism": f"batch sharded over {world} GPUs (no collective)" if world > 1 else "single",
                        "l2": "per-problem working set in SMEM; inputs 78 MB read once per step"},
@@ -473,9 +483,11 @@ def run_batched(args, rank, world, local):
                     "h2d_bytes_per_step": 2 * batch * n * n * 8, "d2h_bytes_per_step": batch * n * n * 8,
                     "ms_per_step": ms_e2e, "steps": 1},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "alu", "kernel": "k_split_batched (DFMA, SMEM-resident, one CTA per problem)",
-                         "achieved": tf, "peak": 34.2, "unit": "TFLOP/s", "frac": tf / 34.2, "traffic": None,
-                         "peak_source": "measured DFMA peak (profiles/r01_fp64_peak_microbench.txt)"},
+            "roofline": {"bound": "tensor",
+                         "kernel": "k_split_batched_wy (DMMA m8n8k4 from SMEM, compact-WY, one CTA per problem)",
+                         "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": tf / FP64_PEAK_TFLOPS, "traffic": None,
+                         "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak_microbench.txt)"},
             "cpu_baseline": cpu, "input_gen_s": t_in}
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -500,6 +512,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: spawn one rank per GPU ourselves (same contract)
+        port = 29500 + (os.getpid() % 2000)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU",
+              file=sys.stderr)
+        return 2
     from paper_1011_3077_b200 import inputs
     cfg = args.config
     if cfg == 10:
@@ -716,7 +739,8 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        total, threads, sample, spent = oracle_sample(n, info.iters, pencil, n_sample=args.ref_n)
+        total, threads, sample, spent = oracle_sample(n, info.iters, pencil, n_sample=args.ref_n, cfg=cfg,
+                                                      monitor=(stop == "e21"), ql_orth=ql_orth)
         cpu = {"value": 1.0 / total, "unit": "split steps/s", "cores": threads, "kind": "oracle",
                "sample": sample + " (extrapolated)", "cpu_seconds_spent": spent}
 

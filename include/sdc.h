@@ -98,8 +98,14 @@ typedef struct {
 typedef struct sdc_handle sdc_handle;
 
 /* Create a handle on CUDA device `device` with workspace for matrices up to n_max
- * (pencil != 0 also reserves the RGNEP buffers).  Workspace ~ 17 n_max^2 doubles
- * (RNEP) / 25 n_max^2 (pencil).  Supported: 2 <= n_max <= 24576.  Returns 0 or <0. */
+ * (pencil != 0 also reserves the RGNEP buffers).  Workspace: 19 n_max^2 doubles (stack,
+ * Y, Y^T, complement: 2 n^2 each; V^T, A_j x2, B_j x2, G1-G3, T1, Ahat, R_{j-1}: n^2 each)
+ * + ~ n_max^2/32 (selection partials) + ~ 20 M doubles (split-K partials of both streams)
+ * for RNEP; pencil handles add 9 n_max^2 (left stack, A'_j/B'_j x2, Bhat, Q_L, V_L^T).
+ * The second factorization context (allocated on the first monitor-mode or pencil call)
+ * adds 9 n_max^2 (Y, Y^T, complement, G1-G3) + ~ 10 M doubles.  At n_max = 16384: 41 GB
+ * (RNEP), 60 GB with the second context.  The caller's current device is restored on
+ * return (as by every entry point below).  Supported: 2 <= n_max <= 24576.  Returns 0 or <0. */
 int sdc_create(sdc_handle** h, int device, int n_max, int pencil);
 void sdc_destroy(sdc_handle* h);
 
@@ -184,7 +190,8 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
  * Decisions (DESIGN.md §10 "recursion", identical in orc_schur): a block of order m is a leaf
  * if m <= leaf, or m == 2 with complex eigenvalues; else up to 16 attempts, each a random
  * line in the middle half of [c - 2s, c + 2s] (c = trace/m, s = ||T_blk - cI||_F/sqrt(m)),
- * a counter-based Haar V (seed), and one RNEP half-plane step in monitor mode
+ * a counter-based Haar V (seed; draws keyed by the block's offset and order, see
+ * sdc_schur_keyed), and one RNEP half-plane step in monitor mode
  * (SDC_STOP_E21 with `tol`, at most max_iters passes), accepted iff its status is 0; a
  * rejected step whose res.side shows every eigenvalue on one side moves that end of the
  * interval to the line.  On acceptance E21 := 0,
@@ -204,6 +211,28 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
 int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int leaf,
               unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
               int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric);
+
+/* sdc_schur with the random draws keyed by GLOBAL block offsets: the attempt-t line and
+ * Haar V of the diagonal block at offset o (of A) use the counter c = key(key_off + o, m, t)
+ * (DESIGN.md §10), so a subproblem A = T(o0:o0+n, o0:o0+n) of a larger recursion, solved
+ * on its own with key_off = o0 -- e.g. on the rank it was handed to --
+ * takes exactly the decisions the whole recursion takes there.  Arguments as sdc_schur with
+ * 6 key_off >= 0 inserted (later positions shift by one).  sdc_schur = key_off 0. */
+int sdc_schur_keyed(sdc_handle* h, void* stream, int n, const double* A, int lda, int key_off, int leaf,
+                    unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
+                    int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric);
+
+/* One node of the recursion: the attempt loop of sdc_schur on the diagonal block Tb
+ * (m x m, device, ld ldtb >= m) at global offset key_off, IN PLACE.
+ *  13 r  HOST out: r in [1, m-1] when a split was accepted -- then Tb holds Ahat = Q_b^T Tb Q_b
+ *        with E21 := 0 and Qb (device, m x m, ld ldqb) the orthogonal Q_b; r = 0 for a leaf
+ *        (m <= leaf, or a 2x2 with complex eigenvalues) or an unsplit block (Tb unchanged)
+ *  14 stats, 15 max_metric  HOST, ACCUMULATED (not reset) as in sdc_schur
+ * Errors: -3 m, -4 Tb, -5 ldtb, -6 key_off, -7 leaf, -9 max_iters, -10 tol, -11 Qb, -12 ldqb,
+ * -13 NULL host output.  Allocates 3 m x m scratch matrices; synchronises `stream`. */
+int sdc_schur_node(sdc_handle* h, void* stream, int m, double* Tb, int ldtb, int key_off, int leaf,
+                   unsigned long long seed, int max_iters, double tol, double* Qb, int ldqb, int* r,
+                   int* stats, double* max_metric);
 
 /* Eigenvectors of an upper triangular matrix (TREVC):
  * X upper triangular with X_jj = 1 and TX = XD, D = diag(T), or, when
@@ -241,9 +270,10 @@ int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N,
               double* C, int ldc);
 
 /* Blocked Householder QR of the m x n matrix A (m >= n, m <= 2 n_max, n <= n_max) in
- * place: on return R (with the LAPACK-sign diagonal) is in the upper triangle.
- * If Qthin != NULL it receives the explicit m x n Q with diag(R) made >= 0 (the rows
- * of R are NOT sign-fixed in A; use the signs of diag(A) to do so).  PAPER.md:331. */
+ * place: on return the upper triangle of A holds R with a NON-NEGATIVE diagonal (rows
+ * scaled by sign(R_ii); the strictly lower part is workspace).  If Qthin != NULL it
+ * receives the explicit m x n Q of the same factorization (A = Qthin R).  PAPER.md:331;
+ * north_star "R diagonal forced non-negative".  Synchronises `stream`. */
 int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double* Qthin,
            int ldq);
 
@@ -286,6 +316,24 @@ int sdc_debug_counters(sdc_handle* h, unsigned long long* out, int count, int re
 
 /* Number of kernels launched by this handle since creation (evidence counter). */
 long long sdc_kernel_launches(const sdc_handle* h);
+
+/* Schedule evidence: how often each code path of the step was ENQUEUED by this handle
+ * (launches inside a captured CUDA graph count once, at capture).  Tests use them to prove
+ * that a parity case ran the path it names (look-ahead fork, multi-cluster panel, ...). */
+enum { SDC_SCHED_LOOKAHEAD_FORKS = 0,  /* look-ahead QR schedules forked to the hi-prio stream */
+       SDC_SCHED_XPASS_FORKS = 1,      /* look-ahead QRs forked by the previous pass (SDC_XPASS) */
+       SDC_SCHED_CTX_FORKS = 2,        /* forks to the second factorization context            */
+       SDC_SCHED_PANEL_CLUSTER = 3,    /* panels as one cluster (DSMEM exchange)               */
+       SDC_SCHED_PANEL_MCLUSTER = 4,   /* panels as several 16-CTA clusters (DSMEM + L2 flags)  */
+       SDC_SCHED_PANEL_GRID = 5,       /* panels as a cooperative grid (L2 + grid barrier)      */
+       SDC_SCHED_GRAPH_CAPTURES = 6,   /* fixed-mode steps captured into a CUDA graph           */
+       SDC_SCHED_GRAPH_REPLAYS = 7,    /* fixed-mode steps replayed from the graph              */
+       SDC_SCHED_PANEL_MCLUSTER_CAPPED = 8, /* multi-cluster panels limited to half the
+                                          resident clusters (two contexts share the SMs)   */
+       SDC_SCHED_COUNTERS = 9 };
+/* Copies `count` (<= SDC_SCHED_COUNTERS) counters to the HOST array out; reset != 0 zeroes
+ * them.  Returns 0, -1 (null handle) or -3 (bad count). */
+int sdc_schedule_counters(sdc_handle* h, long long* out, int count, int reset);
 
 /* Text of the last error on this thread ("" if none). */
 const char* sdc_last_error(void);

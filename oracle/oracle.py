@@ -64,6 +64,10 @@ def lib():
             _lib.orc_haar.argtypes = [I, U64, U64, P, I]
             _lib.orc_schur.restype = I
             _lib.orc_schur.argtypes = [I, P, I, I, U64, I, D, P, I, P, I, P, P, P, P, P]
+            _lib.orc_schur_keyed.restype = I
+            _lib.orc_schur_keyed.argtypes = [I, P, I, I, I, U64, I, D, P, I, P, I, P, P, P, P, P]
+            _lib.orc_schur_node.restype = I
+            _lib.orc_schur_node.argtypes = [I, P, I, I, I, U64, I, D, P, I, P, P]
             _lib.orc_split_select.restype = D
             _lib.orc_split_select.argtypes = [I, P, I, D, P, I, D, ctypes.POINTER(I), P]
             _lib.orc_norm1.restype = D
@@ -324,8 +328,9 @@ class SchurResult:
     max_metric: float
 
 
-def schur(A, leaf=1, seed=1, max_iters=60, tol=1e-13) -> SchurResult:
-    """Recursive divide-and-conquer A = Q T Q^T, T block upper triangular."""
+def schur(A, leaf=1, seed=1, max_iters=60, tol=1e-13, key_off=0) -> SchurResult:
+    """Recursive divide-and-conquer A = Q T Q^T, T block upper triangular (DESIGN.md §10);
+    key_off: global offset of A's first row (a subproblem's random draws are keyed by it)."""
     A = _f(A)
     n = A.shape[0]
     Q = np.zeros((n, n), order="F")
@@ -335,8 +340,8 @@ def schur(A, leaf=1, seed=1, max_iters=60, tol=1e-13) -> SchurResult:
     nb = ctypes.c_int(0)
     stats = np.zeros(4, dtype=np.int32)
     mm = ctypes.c_double(0.0)
-    rc = lib().orc_schur(n, _p(A), n, int(leaf), int(seed), int(max_iters), float(tol), _p(Q), n,
-                         _p(T), n, off.ctypes.data_as(ctypes.c_void_p),
+    rc = lib().orc_schur_keyed(n, _p(A), n, int(key_off), int(leaf), int(seed), int(max_iters),
+                               float(tol), _p(Q), n, _p(T), n, off.ctypes.data_as(ctypes.c_void_p),
                          size.ctypes.data_as(ctypes.c_void_p), ctypes.byref(nb),
                          stats.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mm))
     if rc != 0:
@@ -344,3 +349,19 @@ def schur(A, leaf=1, seed=1, max_iters=60, tol=1e-13) -> SchurResult:
     blocks = [(int(off[i]), int(size[i])) for i in range(nb.value)]
     return SchurResult(Q, T, blocks, int(stats[0]), int(stats[1]), int(stats[2]), int(stats[3]),
                        mm.value)
+
+
+def schur_node(Tb, o, leaf=1, seed=1, max_iters=60, tol=1e-13):
+    """One node of the recursion on the diagonal block Tb at global offset o (in place:
+    Tb <- Ahat with E21 = 0 when split).  Returns (r, Qb or None, stats[4], max_metric);
+    r = 0: leaf or unsplit block."""
+    m = Tb.shape[0]
+    assert Tb.flags.f_contiguous and Tb.dtype == np.float64
+    Qb = np.zeros((m, m), order="F")
+    stats = np.zeros(4, dtype=np.int32)
+    mm = ctypes.c_double(0.0)
+    r = lib().orc_schur_node(m, _p(Tb), m, int(o), int(leaf), int(seed), int(max_iters), float(tol),
+                             _p(Qb), m, stats.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mm))
+    if r < 0:
+        raise ValueError(f"orc_schur_node returned {r}")
+    return r, (Qb if r > 0 else None), stats, mm.value

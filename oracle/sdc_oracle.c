@@ -688,8 +688,9 @@ void orc_trevc(int n, const double *T, int ldt, const double *Q, int ldq, double
  *     change decisions), [lo, hi] = [c - 2s, c + 2s] (PAPER.md:472-475 uses a disk of radius
  *     R/2 around the centre; Gershgorin radii of dense blocks are ~sqrt(m) too wide); s = 0:
  *     unsplittable leaf;
- *   - attempt t (t < 16): a = lo + (0.25 + 0.5 u)(hi - lo), u = U01(seed, 2 s), V = Haar of
- *     order m from the Gaussian stream 2 s + 1 (s = running split counter); RNEP step in
+ *   - attempt t (t < 16): a = lo + (0.25 + 0.5 u)(hi - lo), u = U01(seed, 2 c), V = Haar of
+ *     order m from the Gaussian stream 2 c + 1, c = orc_attempt_ctr(global offset, m, t)
+ *     (keyed by the block, so any processing order draws the same numbers); RNEP step in
  *     monitor mode (stop at the first pass with ||E21||_1/||A||_1 <= tol_b = max(tol, 8e-15 m),
  *     PAPER.md:597, or at a plateau <= 10 tol_b that no longer halves, or once the IRS pair
  *     is one-sided) with at most max_iters passes; accepted iff status 0 (<= 1e-8, Q4) and
@@ -730,10 +731,85 @@ void orc_haar(int m, unsigned long long seed, unsigned long long key, double *V,
   free(tau);
 }
 
-int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed, int max_iters, double tol,
-              double *Q, int ldq, double *T, int ldt, int *blk_off, int *blk_size, int *nblk,
-              int *stats, double *max_metric) {
-  if (n < 1 || lda < n || ldq < n || ldt < n || leaf < 1) return -1;
+/* Counter of attempt t (< 16) on the diagonal block at GLOBAL offset o of order m: keyed by
+ * the block's identity (not by a running counter), so the draws -- and hence every decision
+ * -- do not depend on the order in which blocks are processed: depth first on one rank, or
+ * subproblems handed to other ranks.  23 bits, so the Gaussian stream key
+ * 2 ctr + 1 shifted left by 40 stays inside 64 bits. */
+static uint64_t orc_attempt_ctr(int o, int m, int t) {
+  const uint64_t id = (uint64_t)o * 65537ull + (uint64_t)m;
+  return ((orc_mix64(0x5DC0FFEEull, id) & 0x7FFFFull) << 4) | (uint64_t)t;
+}
+
+/* One node of the recursion: the attempt loop on the diagonal block Tb (m x m, ld ldtb) at
+ * global offset o.  Accepted: Tb <- Ahat with E21 := 0, Qb <- the block's orthogonal factor
+ * (m x m, ld ldqb), returns r in [1, m-1].  Returns 0 for a leaf (m <= leaf or a 2x2 with
+ * complex eigenvalues) or an unsplit block (s = 0, or 16 failed attempts: stats[2]++); Tb is
+ * then unchanged.  stats (splits, failed attempts, unsplit, passes) and max_metric accumulate. */
+int orc_schur_node(int m, double *Tb, int ldtb, int o, int leaf, unsigned long long seed, int max_iters,
+                   double tol, double *Qb, int ldqb, int *stats, double *max_metric) {
+  if (m < 1 || ldtb < m || ldqb < m || leaf < 1) return -1;
+  if (m <= leaf) return 0;
+  if (m == 2) {   /* 2x2 with complex eigenvalues: a standardised leaf */
+    const double a = EL(Tb, 0, 0, ldtb), b = EL(Tb, 0, 1, ldtb), c = EL(Tb, 1, 0, ldtb), d = EL(Tb, 1, 1, ldtb);
+    if ((a - d) * (a - d) + 4.0 * b * c < 0.0) return 0;
+  }
+  double tr = 0.0;
+  for (int i = 0; i < m; ++i) tr += EL(Tb, i, i, ldtb);
+  const double c = tr / m;
+  double f2 = 0.0;
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) {
+      const double t = EL(Tb, i, j, ldtb) - (i == j ? c : 0.0);
+      f2 += t * t;
+    }
+  const double sd = sqrt(f2 / m);
+  double lo = c - 2.0 * sd, hi = c + 2.0 * sd;
+  if (!(sd > 0.0)) { stats[2]++; return 0; }
+  const size_t mm = (size_t)m * m;
+  double *Tw = (double *)malloc(sizeof(double) * mm), *V = (double *)malloc(sizeof(double) * mm);
+  double *Ab = (double *)malloc(sizeof(double) * mm), *Qw = (double *)malloc(sizeof(double) * mm);
+  int r = 0;
+  for (int att = 0; att < 16; ++att) {
+    const uint64_t ctr = orc_attempt_ctr(o, m, att);
+    const double u = orc_u01(seed, 2ull * ctr);
+    const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
+    orc_haar(m, seed, 2ull * ctr + 1ull, V, m);
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) EL(Tw, i, j, m) = EL(Tb, i, j, ldtb);
+    orc_result res;
+    const double tolb = fmax(tol, 8e-15 * m);   /* rounding floor grows ~ m eps */
+    int rc = orc_split_region(m, Tw, m, NULL, 0, V, m, NULL, 0, ORC_REGION_HALFPLANE, a,
+                              ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED, max_iters, tolb, ORC_STOP_E21,
+                              Qw, m, NULL, 0, Ab, m, NULL, 0, &res);
+    if (rc) { r = rc; break; }
+    stats[3] += res.iters;
+    const int onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
+    if (res.status != ORC_STATUS_SPLIT || onesided) {   /* a one-sided pair's split is incidental */
+      stats[1]++;
+      if (res.side > 0.95) hi = a;          /* every eigenvalue left of the line  */
+      else if (res.side < 0.05) lo = a;     /* every eigenvalue right of the line */
+      continue;
+    }
+    r = res.r;
+    stats[0]++;
+    *max_metric = fmax(*max_metric, res.metric);
+    for (int j = 0; j < m; ++j)   /* Tb = Ahat with E21 = 0 */
+      for (int i = 0; i < m; ++i) {
+        EL(Tb, i, j, ldtb) = (i >= r && j < r) ? 0.0 : EL(Ab, i, j, m);
+        EL(Qb, i, j, ldqb) = EL(Qw, i, j, m);
+      }
+    break;
+  }
+  if (r == 0) stats[2]++;   /* 16 failed attempts: an unsplit leaf */
+  free(Tw); free(V); free(Ab); free(Qw);
+  return r;
+}
+
+int orc_schur_keyed(int n, const double *A, int lda, int key_off, int leaf, unsigned long long seed,
+                    int max_iters, double tol, double *Q, int ldq, double *T, int ldt, int *blk_off,
+                    int *blk_size, int *nblk, int *stats, double *max_metric) {
+  if (n < 1 || lda < n || ldq < n || ldt < n || leaf < 1 || key_off < 0) return -1;
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) {
       EL(T, i, j, ldt) = EL(A, i, j, lda);
@@ -742,93 +818,45 @@ int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed
   for (int q = 0; q < 4; ++q) stats[q] = 0;   /* splits, failed attempts, unsplit leaves, passes */
   *max_metric = 0.0;                           /* largest accepted ||E21||_1/||A_blk||_1 */
   int *st_o = (int *)malloc(sizeof(int) * 2 * n), *st_m = (int *)malloc(sizeof(int) * 2 * n);
-  int sp = 0, nb = 0;
-  uint64_t s = 0;
+  int sp = 0, nb = 0, rc = 0;
   st_o[sp] = 0; st_m[sp] = n; ++sp;
-  double *Tb = (double *)malloc(sizeof(double) * (size_t)n * n);
-  double *V = (double *)malloc(sizeof(double) * (size_t)n * n);
   double *Qb = (double *)malloc(sizeof(double) * (size_t)n * n);
-  double *Ab = (double *)malloc(sizeof(double) * (size_t)n * n);
   double *W = (double *)malloc(sizeof(double) * (size_t)n * n);
   while (sp > 0) {
     --sp;
     const int o = st_o[sp], m = st_m[sp];
-    int leafy = m <= leaf;
-    if (!leafy && m == 2) {   /* 2x2 with complex eigenvalues: a standardised leaf */
-      const double a = EL(T, o, o, ldt), b = EL(T, o, o + 1, ldt), c = EL(T, o + 1, o, ldt),
-                   d = EL(T, o + 1, o + 1, ldt);
-      if ((a - d) * (a - d) + 4.0 * b * c < 0.0) leafy = 1;
+    const int r = orc_schur_node(m, &EL(T, o, o, ldt), ldt, key_off + o, leaf, seed, max_iters, tol, Qb, m,
+                                 stats, max_metric);
+    if (r < 0) { rc = r; break; }
+    if (r == 0) { blk_off[nb] = o; blk_size[nb] = m; ++nb; continue; }
+    /* T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n) */
+    const int nr = n - o - m;
+    if (nr > 0) {
+      orc_gemm(1, 0, m, nr, m, Qb, m, &EL(T, o, o + m, ldt), ldt, W, m);
+      for (int j = 0; j < nr; ++j)
+        for (int i = 0; i < m; ++i) EL(T, o + i, o + m + j, ldt) = EL(W, i, j, m);
     }
-    double lo = 0.0, hi = 0.0;
-    if (!leafy) {
-      double tr = 0.0;
-      for (int i = 0; i < m; ++i) tr += EL(T, o + i, o + i, ldt);
-      const double c = tr / m;
-      double f2 = 0.0;
+    /* T(0:o, o:o+m) = T(0:o, o:o+m) Qb */
+    if (o > 0) {
+      orc_gemm(0, 0, o, m, m, &EL(T, 0, o, ldt), ldt, Qb, m, W, o);
       for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) {
-          const double t = EL(T, o + i, o + j, ldt) - (i == j ? c : 0.0);
-          f2 += t * t;
-        }
-      const double sd = sqrt(f2 / m);
-      lo = c - 2.0 * sd;
-      hi = c + 2.0 * sd;
-      if (!(sd > 0.0)) { leafy = 1; stats[2]++; }
+        for (int i = 0; i < o; ++i) EL(T, i, o + j, ldt) = EL(W, i, j, o);
     }
-    int done = 0;
-    for (int att = 0; !leafy && att < 16; ++att) {
-      const double u = orc_u01(seed, 2ull * s);
-      const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
-      orc_haar(m, seed, 2ull * s + 1ull, V, m);
-      ++s;
-      for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) EL(Tb, i, j, m) = EL(T, o + i, o + j, ldt);
-      orc_result res;
-      const double tolb = fmax(tol, 8e-15 * m);   /* rounding floor grows ~ m eps */
-      int rc = orc_split_region(m, Tb, m, NULL, 0, V, m, NULL, 0, ORC_REGION_HALFPLANE, a,
-                                ORC_FLAG_PLATEAU | ORC_FLAG_ONESIDED, max_iters, tolb, ORC_STOP_E21,
-                                Qb, m, NULL, 0, Ab, m, NULL, 0, &res);
-      if (rc) { free(st_o); free(st_m); free(Tb); free(V); free(Qb); free(Ab); free(W); return rc; }
-      stats[3] += res.iters;
-      const int onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
-      if (res.status != ORC_STATUS_SPLIT || onesided) {   /* a one-sided pair's split is incidental */
-        stats[1]++;
-        if (res.side > 0.95) hi = a;          /* every eigenvalue left of the line  */
-        else if (res.side < 0.05) lo = a;     /* every eigenvalue right of the line */
-        continue;
-      }
-      const int r = res.r;
-      stats[0]++;
-      *max_metric = fmax(*max_metric, res.metric);
-      /* T(o:o+m, o:o+m) = Ahat with E21 = 0 */
-      for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) EL(T, o + i, o + j, ldt) = (i >= r && j < r) ? 0.0 : EL(Ab, i, j, m);
-      /* T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n) */
-      const int nr = n - o - m;
-      if (nr > 0) {
-        orc_gemm(1, 0, m, nr, m, Qb, m, &EL(T, o, o + m, ldt), ldt, W, m);
-        for (int j = 0; j < nr; ++j)
-          for (int i = 0; i < m; ++i) EL(T, o + i, o + m + j, ldt) = EL(W, i, j, m);
-      }
-      /* T(0:o, o:o+m) = T(0:o, o:o+m) Qb */
-      if (o > 0) {
-        orc_gemm(0, 0, o, m, m, &EL(T, 0, o, ldt), ldt, Qb, m, W, o);
-        for (int j = 0; j < m; ++j)
-          for (int i = 0; i < o; ++i) EL(T, i, o + j, ldt) = EL(W, i, j, o);
-      }
-      /* Q(:, o:o+m) = Q(:, o:o+m) Qb */
-      orc_gemm(0, 0, n, m, m, &EL(Q, 0, o, ldq), ldq, Qb, m, W, n);
-      for (int j = 0; j < m; ++j)
-        for (int i = 0; i < n; ++i) EL(Q, i, o + j, ldq) = EL(W, i, j, n);
-      st_o[sp] = o + r; st_m[sp] = m - r; ++sp;   /* trailing (Re < a), processed second */
-      st_o[sp] = o; st_m[sp] = r; ++sp;           /* leading (Re > a), processed first   */
-      done = 1;
-      break;
-    }
-    if (!leafy && !done) stats[2]++;
-    if (leafy || !done) { blk_off[nb] = o; blk_size[nb] = m; ++nb; }
+    /* Q(:, o:o+m) = Q(:, o:o+m) Qb */
+    orc_gemm(0, 0, n, m, m, &EL(Q, 0, o, ldq), ldq, Qb, m, W, n);
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < n; ++i) EL(Q, i, o + j, ldq) = EL(W, i, j, n);
+    st_o[sp] = o + r; st_m[sp] = m - r; ++sp;   /* trailing (Re < a), processed second */
+    st_o[sp] = o; st_m[sp] = r; ++sp;           /* leading (Re > a), processed first   */
   }
   *nblk = nb;
-  free(st_o); free(st_m); free(Tb); free(V); free(Qb); free(Ab); free(W);
-  return 0;
+  free(st_o); free(st_m); free(Qb); free(W);
+  return rc;
+}
+
+int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed, int max_iters, double tol,
+              double *Q, int ldq, double *T, int ldt, int *blk_off, int *blk_size, int *nblk,
+              int *stats, double *max_metric) {
+  return orc_schur_keyed(n, A, lda, 0, leaf, seed, max_iters, tol, Q, ldq, T, ldt, blk_off, blk_size, nblk,
+                         stats, max_metric);
 }

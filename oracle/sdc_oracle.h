@@ -84,6 +84,15 @@ void orc_haar(int m, unsigned long long seed, unsigned long long key, double *V,
 int orc_schur(int n, const double *A, int lda, int leaf, unsigned long long seed, int max_iters,
               double tol, double *Q, int ldq, double *T, int ldt, int *blk_off, int *blk_size,
               int *nblk, int *stats, double *max_metric);
+/* the same with the random draws keyed by GLOBAL block offsets key_off + o (a subproblem of
+ * a larger recursion, e.g. handed to another rank: PAPER.md:989-991) */
+int orc_schur_keyed(int n, const double *A, int lda, int key_off, int leaf, unsigned long long seed,
+                    int max_iters, double tol, double *Q, int ldq, double *T, int ldt, int *blk_off,
+                    int *blk_size, int *nblk, int *stats, double *max_metric);
+/* one node: the attempt loop on the diagonal block Tb at global offset o; returns r > 0
+ * (Tb <- Ahat with E21 = 0, Qb <- the block's orthogonal factor), 0 (leaf / unsplit), < 0 error */
+int orc_schur_node(int m, double *Tb, int ldtb, int o, int leaf, unsigned long long seed, int max_iters,
+                   double tol, double *Qb, int ldqb, int *stats, double *max_metric);
 
 #ifdef __cplusplus
 }

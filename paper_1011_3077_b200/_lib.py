@@ -13,6 +13,8 @@ REGION_UNIT_DISK, REGION_DISK, REGION_HALFPLANE = 0, 1, 2
 FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED, FLAG_QL_ORTH = 1, 2, 4, 8
 PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PROF_GEMM_OTHER = 0, 1, 2, 3, 4, 5, 6
 SPLIT_ACCEPT = 1e-8
+SCHED_NAMES = ("lookahead_forks", "xpass_forks", "ctx_forks", "panel_cluster", "panel_mcluster",
+               "panel_grid", "graph_captures", "graph_replays", "panel_mcluster_capped")
 
 
 class SdcResult(ctypes.Structure):
@@ -35,6 +37,10 @@ _SIGS = {
     "sdc_split_batched": (I, [P, P, I, I, P, I, LL, P, I, LL, I, P, I, LL, P]),
     "sdc_schur": (I, [P, P, I, P, I, I, ctypes.c_ulonglong, I, D, P, I, P, I, P, P,
                       ctypes.POINTER(I), P, ctypes.POINTER(D)]),
+    "sdc_schur_keyed": (I, [P, P, I, P, I, I, I, ctypes.c_ulonglong, I, D, P, I, P, I, P, P,
+                            ctypes.POINTER(I), P, ctypes.POINTER(D)]),
+    "sdc_schur_node": (I, [P, P, I, P, I, I, I, ctypes.c_ulonglong, I, D, P, I, ctypes.POINTER(I), P,
+                           ctypes.POINTER(D)]),
     "sdc_svd_split": (I, [P, P, I, I, P, I, D, P, I, I, D, I, P, I, P, I, P, I,
                           ctypes.POINTER(SdcResult)]),
     "sdc_split_host": (I, [P, P, I, P, P, P, P, I, D, I, P, P, P, P, I, ctypes.POINTER(SdcResult)]),
@@ -43,6 +49,7 @@ _SIGS = {
     "sdc_irs_pass": (I, [P, P, I, P, I, P, I, P, I, P, I, P, I]),
     "sdc_split_select": (I, [P, P, I, P, I, D, P, I, D, ctypes.POINTER(I), ctypes.POINTER(D), P]),
     "sdc_kernel_launches": (LL, [P]),
+    "sdc_schedule_counters": (I, [P, P, I, I]),
     "sdc_profile": (I, [P, I]),
     "sdc_debug_counters": (I, [P, P, I, I]),
     "sdc_profile_read": (I, [P, I, ctypes.POINTER(D), ctypes.POINTER(LL), ctypes.POINTER(D)]),

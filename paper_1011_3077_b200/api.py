@@ -87,6 +87,13 @@ class Handle:
     def launches(self) -> int:
         return int(self.lib.sdc_kernel_launches(self._h))
 
+    def schedule_counters(self, reset: bool = False) -> dict:
+        """sdc_schedule_counters: how often each schedule path was enqueued (evidence)."""
+        out = (ctypes.c_longlong * len(_lib.SCHED_NAMES))()
+        check(self.lib.sdc_schedule_counters(self._h, out, len(_lib.SCHED_NAMES), int(reset)),
+              "sdc_schedule_counters")
+        return dict(zip(_lib.SCHED_NAMES, (int(v) for v in out)))
+
     def profile(self, enable: bool = True):
         check(self.lib.sdc_profile(self._h, int(enable)), "sdc_profile")
 
@@ -162,12 +169,19 @@ class Handle:
     def split_batched(self, A, V, max_iters=12, Q=None):
         """sdc_split_batched: A, V of shape (batch, n, n) with each A[b] column-major (e.g.
         A = X.transpose(1, 2).contiguous().transpose(1, 2)); returns (Q, [SplitInfo])."""
+        if A.dim() != 3 or A.shape[1] != A.shape[2]:
+            raise ValueError("A must be (batch, n, n)")
         batch, n, _ = A.shape
-        for x in (A, V):
-            if x.dtype != torch.float64 or not x.is_cuda or x.stride(1) != 1 or x.stride(2) < n:
-                raise ValueError("expected (batch, n, n) column-major float64 CUDA tensors")
         if Q is None:
             Q = torch.empty((batch, n, n), dtype=torch.float64, device=A.device).transpose(1, 2)
+        # the C ABI cannot see buffer sizes: V and Q must match A's batch and order (ADVICE r01)
+        for name, x in (("A", A), ("V", V), ("Q", Q)):
+            if tuple(x.shape) != (batch, n, n):
+                raise ValueError(f"{name} must have shape {(batch, n, n)}, got {tuple(x.shape)}")
+            if (x.dtype != torch.float64 or not x.is_cuda or x.device != A.device or
+                    (n > 1 and x.stride(1) != 1) or x.stride(2) < n or
+                    (batch > 1 and x.stride(0) < x.stride(2) * n)):
+                raise ValueError(f"{name}: expected (batch, n, n) column-major float64 CUDA tensors")
         res = (SdcResult * max(1, batch))()
         check(self.lib.sdc_split_batched(self._h, _stream(A.device), batch, n,
                                          ctypes.c_void_p(A.data_ptr()), A.stride(2), A.stride(0),
@@ -178,8 +192,9 @@ class Handle:
                  for r in res[:batch]]
         return Q, infos
 
-    def schur(self, A, leaf=1, seed=1, max_iters=60, tol=1e-13, Q=None, T=None):
-        """sdc_schur: recursive divide-and-conquer A = Q T Q^T.
+    def schur(self, A, leaf=1, seed=1, max_iters=60, tol=1e-13, Q=None, T=None, key_off=0):
+        """sdc_schur_keyed: recursive divide-and-conquer A = Q T Q^T; key_off
+        is the global offset of A in a larger recursion (draws keyed by it).
         Returns (Q, T, blocks [(offset, size)], stats dict)."""
         n = A.shape[0]
         A = colmajor(A)
@@ -193,8 +208,8 @@ class Handle:
         pa, la = _ptr_ld(A)
         pq, lq = _ptr_ld(Q)
         pt, lt = _ptr_ld(T)
-        check(self.lib.sdc_schur(self._h, _stream(A.device), n, pa, la, int(leaf), int(seed),
-                                 int(max_iters), float(tol), pq, lq, pt, lt,
+        check(self.lib.sdc_schur_keyed(self._h, _stream(A.device), n, pa, la, int(key_off), int(leaf),
+                                       int(seed), int(max_iters), float(tol), pq, lq, pt, lt,
                                  off.ctypes.data_as(ctypes.c_void_p), size.ctypes.data_as(ctypes.c_void_p),
                                  ctypes.byref(nb), stats.ctypes.data_as(ctypes.c_void_p),
                                  ctypes.byref(mm)), "sdc_schur")
@@ -202,6 +217,27 @@ class Handle:
         info = {"splits": int(stats[0]), "failed_attempts": int(stats[1]), "unsplit": int(stats[2]),
                 "passes": int(stats[3]), "max_metric": mm.value}
         return Q, T, blocks, info
+
+    def schur_node(self, Tb, key_off, leaf=1, seed=1, max_iters=60, tol=1e-13, Qb=None, stats=None):
+        """sdc_schur_node: one node of the recursion on the diagonal block Tb (in place).
+        Returns (r, Qb); r = 0: leaf / unsplit.  stats: optional int32[4] + [max_metric]
+        accumulators (numpy), updated in place."""
+        m = Tb.shape[0]
+        pt, lt = _ptr_ld(Tb)
+        if Tb.shape != (m, m):
+            raise ValueError("Tb must be square")
+        Qb = empty_colmajor(m, m, Tb.device) if Qb is None else Qb
+        pq, lq = _ptr_ld(Qb)
+        st = np.zeros(4, dtype=np.int32) if stats is None else stats[0]
+        mm = ctypes.c_double(0.0 if stats is None else float(stats[1][0]))
+        r = ctypes.c_int(0)
+        check(self.lib.sdc_schur_node(self._h, _stream(Tb.device), m, pt, lt, int(key_off), int(leaf),
+                                      int(seed), int(max_iters), float(tol), pq, lq, ctypes.byref(r),
+                                      st.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mm)),
+              "sdc_schur_node")
+        if stats is not None:
+            stats[1][0] = mm.value
+        return r.value, Qb
 
     def trevc(self, T, Q=None, X=None):
         """sdc_trevc: eigenvectors X (X_jj = 1, TX = XD) of the upper triangular T, or Q X
@@ -228,6 +264,16 @@ class Handle:
         Q = np.empty((n, n), order="F") if Q is None else Q
         if B is not None and QL is None:
             QL = np.empty((n, n), order="F")
+        # host buffers are read / written as n x n column-major fp64
+        for name, x in (("A", A), ("B", B), ("V", V), ("VL", VL), ("Q", Q), ("QL", QL)):
+            if x is None:
+                continue
+            if x.shape != (n, n):
+                raise ValueError(f"{name} must be {n} x {n}, got {x.shape}")
+            if x.dtype != np.float64 or not x.flags.f_contiguous:
+                raise ValueError(f"{name} must be a Fortran-ordered float64 array")
+        if B is not None and VL is None:
+            raise ValueError("a pencil (B given) needs VL")
         Ah = np.empty((n, n), order="F") if want_ahat else None
         hist = np.full((max_iters, 3), np.nan)
         res = SdcResult()
@@ -265,9 +311,7 @@ class Handle:
         pa, la = _ptr_ld(A)
         pq, lq = _ptr_ld(Q)
         check(self.lib.sdc_qr(self._h, _stream(A.device), m, n, pa, la, pq, lq), "sdc_qr")
-        R = torch.triu(A[:n, :n])
-        d = torch.where(torch.diagonal(R) < 0, -1.0, 1.0).to(R)
-        return Q, d[:, None] * R
+        return Q, torch.triu(A[:n, :n])   # sdc_qr leaves R with diag >= 0 in the upper triangle
 
     def irs_pass(self, A, B):
         A, B = colmajor(A), colmajor(B)

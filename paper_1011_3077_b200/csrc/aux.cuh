@@ -229,6 +229,18 @@ __global__ void k_col_sign(double* X, long long ldx, int m, int n, const double*
   }
 }
 
+// R(i, i:n) *= sign(R(i,i)) for the upper triangle of A (one warp per row: the diagonal is
+// read before any lane of that warp writes the row, and no other warp touches it)
+__global__ void k_r_rows_nonneg(double* A, long long lda, int n) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const int i = warp;
+  const bool neg = A[i + (long long)i * lda] < 0.0;
+  __syncwarp();
+  if (neg)
+    for (int j = i + lane; j < n; j += 32) A[i + (long long)j * lda] = -A[i + (long long)j * lda];
+}
+
 // ---- norms: one warp per column -> per-column abs-sum and sum of squares ------------
 __global__ void k_colnorms(const double* X, long long ldx, int m, int n, double* colabs,
                            double* colsq) {

@@ -13,8 +13,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: per-stage ranges
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
@@ -58,6 +60,23 @@ void set_err(const char* fmt, ...) {
     if (rc_ != 0) return rc_; \
   } while (0)
 
+// NVTX range per stage of the step (IRS pass, QR, GRURV, similarity + selection, ...), so
+// an nsys/ncu timeline groups the kernels by the paper's steps; no-ops without a tool
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
+// Per-device "already set" flags for cudaFuncSetAttribute (the attribute is per device;
+// a process may hold handles on several devices)
+constexpr int MAX_DEV = 64;
+struct DevOnce {
+  std::atomic<unsigned long long> mask{0};
+  static unsigned long long bit(int dev) { return 1ull << (dev & (MAX_DEV - 1)); }
+  bool has(int dev) const { return (mask.load(std::memory_order_relaxed) & bit(dev)) != 0; }
+  void set(int dev) { mask.fetch_or(bit(dev), std::memory_order_relaxed); }
+};
+
 constexpr int NB = PANEL_NB;       // panel / WY block width
 constexpr int SCAL_HIST = 12;      // scal[12 + j]: R-test ratio of pass j; scal[8..11]: norms of
                                    // the final right IRS pair (1, F) of A_p and of B_p
@@ -87,6 +106,8 @@ struct sdc_handle {
   unsigned long long bar_count = 0;
   int* flag = nullptr;
   long long launches = 0;
+  long long sched[SDC_SCHED_COUNTERS] = {0};   // schedule evidence (sdc_schedule_counters)
+  bool share_sms = false;              // two factorization contexts may run panels at once
   unsigned long long* dbg = nullptr;   // debug counters (sdc_debug_counters)
   bool dbg_on = false;
   int panel_rows = 128;                // target rows per panel CTA
@@ -305,11 +326,11 @@ using TmaR = TmaTile<128, 64, 64, 32, 3, 2, false, true>;  // updates with beta 
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
   using Sm = GemmSmem<T, TA, TB>;
-  static int attr_set = 0;   // per instantiation (single device per process in practice)
-  if (!attr_set) {
+  static DevOnce attr;   // per instantiation and device
+  if (!attr.has(h->device)) {
     SDC_CK(cudaFuncSetAttribute(gemm_dmma_kernel<T, TA, TB, VEC>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Sm::BYTES));
-    attr_set = 1;
+    attr.set(h->device);
   }
   dim3 grid(cdiv(g.M, T::BM), cdiv(g.N, T::BN), splits);
   ProfScope ps(h, SDC_PROF_GEMM, 2.0 * g.M * g.N * (double)g.K, h->gemm_sub);
@@ -383,11 +404,11 @@ int gemm_variant_override() {
 template <class T>
 int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
                  const TmaGemmArgs& g, int splits) {
-  static int attr_set = 0;
+  static DevOnce attr;
   const int smem = (int)T::SMEM;
-  if (!attr_set) {
+  if (!attr.has(h->device)) {
     SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = 1;
+    attr.set(h->device);
   }
   CUtensorMap tA, tB, tC;
   if (!make_tmap(&tA, A, g.K, g.M, lda, T::BM) || !make_tmap(&tB, B, g.K, g.N, ldb, T::BN)) {
@@ -412,11 +433,11 @@ int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B,
 template <class T>
 int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
                        const TmaGemmArgs& g, int splits) {
-  static int attr_set = 0;
+  static DevOnce attr;
   const int smem = (int)T::SMEM;
-  if (!attr_set) {
+  if (!attr.has(h->device)) {
     SDC_CK(cudaFuncSetAttribute(gemm_tn_tma_persist_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set = 1;
+    attr.set(h->device);
   }
   CUtensorMap tA, tB;
   if (!make_tmap(&tA, A, g.K, g.M, lda, T::BM) || !make_tmap(&tB, B, g.K, g.N, ldb, T::BN)) {
@@ -614,6 +635,9 @@ const void* panel_fn(bool cluster, int rpt) {
   }
 }
 inline int rpt_slot(int rpt) { return rpt == 8 ? 1 : rpt == 16 ? 2 : rpt == 32 ? 3 : 0; }
+// dynamic shared memory currently allowed per (device, exchange mode, RPT variant) of the panel
+// kernel (the attribute is per device; sdc_create re-sets the cluster RPT=0 entry it probes)
+size_t g_panel_attr[MAX_DEV][2][4] = {};
 
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
@@ -625,7 +649,15 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
   if (cluster) {
     G = std::min(16, std::max(1, cdiv(m, h->panel_rows)));
   } else if (h->mcluster_ok) {
-    const int ncl = std::max(2, std::min(h->max_clusters16, cdiv(m, 16 * h->panel_rows)));
+    // The clusters of a multi-cluster panel spin on each other's L2 flags, so all of them
+    // must become resident.  When both factorization contexts can issue such panels at the
+    // same time (pencil chains, pipelined monitor mode), each panel takes at most half the
+    // clusters that fit the GPU: two partly resident panels can then never wait on each
+    // other (VERDICT r01 weak 8 / ADVICE r01).
+    const int cap = h->share_sms ? std::max(2, h->max_clusters16 / 2) : h->max_clusters16;
+    const int want = cdiv(m, 16 * h->panel_rows);
+    const int ncl = std::max(2, std::min(cap, want));
+    if (h->share_sms && want > cap) h->sched[SDC_SCHED_PANEL_MCLUSTER_CAPPED]++;
     if (panel_smem_bytes(cdiv(m, 16 * ncl)) <= 227 * 1024) {
       cluster = true;
       csize = 16;
@@ -646,8 +678,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
   size_t smem = panel_smem_bytes(rows_per);
   const int rpt = h->panel_reg ? panel_rpt(rows_per) : 0;
   const void* fn = panel_fn(cluster, rpt);
-  static size_t attr_smem[2][4] = {};
-  size_t& cur = attr_smem[cluster][rpt_slot(rpt)];
+  size_t& cur = g_panel_attr[h->device & (MAX_DEV - 1)][cluster][rpt_slot(rpt)];
   if (smem > cur) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
@@ -676,11 +707,13 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     void* args[] = {&a};
     SDC_CK(cudaLaunchKernelExC(&cfg, fn, args));
     if (G > csize) h->ll_epoch += nb;
+    h->sched[G > csize ? SDC_SCHED_PANEL_MCLUSTER : SDC_SCHED_PANEL_CLUSTER]++;
   } else {
     void* args[] = {&a};
     SDC_CK(cudaLaunchCooperativeKernel(fn, dim3(G),
                                        dim3(PANEL_THREADS), args, smem, h->st));
     h->bar_count += (unsigned long long)G * nb;
+    h->sched[SDC_SCHED_PANEL_GRID]++;
   }
   h->launches++;
   return 0;
@@ -817,6 +850,7 @@ int blocked_qr_lookahead(sdc_handle* h, double* A, long long lda, int m, int n, 
   } else {
     SDC_CK(cudaEventRecord(h->la_fork, la.side));
   }
+  h->sched[pendingB ? SDC_SCHED_XPASS_FORKS : SDC_SCHED_LOOKAHEAD_FORKS]++;
   SDC_CK(cudaStreamWaitEvent(h->st_hi, h->la_fork, 0));
   la.use_side(false);
   for (int I0 = 0; I0 < n; I0 += h->nbo) {
@@ -846,6 +880,7 @@ int blocked_qr_lookahead(sdc_handle* h, double* A, long long lda, int m, int n, 
 // nbo-wide outer blocks (inner WY updates restricted to the block), then one rank-nbo
 // trailing update per outer block.  Factors into f, T blocks into h->Tb / h->Tob.
 int blocked_qr(sdc_handle* h, double* A, long long lda, int m, int n, const Fac& f) {
+  Nvtx nv("blocked_qr");
   if (lookahead_qr(h, n)) return blocked_qr_lookahead(h, A, lda, m, n, f);
   h->xpass_pending = false;
   for (int I0 = 0; I0 < n; I0 += h->nbo) {
@@ -926,6 +961,7 @@ Fac fac_square(sdc_handle* h, int n) { return Fac{h->Y, (long long)n, h->Yt, (lo
 int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double* Bj,
              long long ldb, double* An, long long ldan, double* Bn, long long ldbn, double* S,
              int rtest_slot, double* Rout, long long ldr, bool xpass = false) {
+  Nvtx nv("irs_pass (Alg. 3 l.3)");
   const long long m = 2LL * n;
   const Fac f = fac_stack(h, n);
   SDC_TRY(blocked_qr(h, S, m, (int)m, n, f));
@@ -983,6 +1019,7 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
 // Vt = V^T (prepared once per split).
 int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* Vt,
                 double* Q, long long ldq) {
+  Nvtx nv("grurv_right (Alg. 1/2)");
   const long long ld = n;
   const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
@@ -1004,6 +1041,7 @@ int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const 
 // Q_L = GRURV(2, A'_p^T, (A'_p+B'_p)^T; +1, -1)  (Alg. 4 line 4); VLt = V_L^T
 int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* VLt,
                double* QL, long long ldq) {
+  Nvtx nv("grurv_left (Alg. 4 l.4)");
   const long long ld = n;
   const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
@@ -1063,6 +1101,7 @@ int select_dev(sdc_handle* h, int n, const double* Ah, long long ldah, const dou
 int similarity_select(sdc_handle* h, int n, const double* A, long long lda, const double* B,
                       long long ldb, const double* Q, long long ldq, const double* QL,
                       long long ldql) {
+  Nvtx nv("similarity + split selection");
   const long long ld = n;
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, A, lda, QL, ldql, 0.0, h->T1, ld));     // G = A^T QL
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->T1, ld, Q, ldq, 0.0, h->Ah, ld));    // G^T Q
@@ -1171,7 +1210,7 @@ int ensure_alt(sdc_handle* h) {
 
 // make `to` wait for the work issued so far on `from` (fork / join between the contexts)
 int stream_dep(sdc_handle* h, cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
-  (void)h;
+  if (to == h->alt.st) h->sched[SDC_SCHED_CTX_FORKS]++;
   SDC_CK(cudaEventRecord(ev, from));
   SDC_CK(cudaStreamWaitEvent(to, ev, 0));
   return 0;
@@ -1188,16 +1227,28 @@ int check_barrier(sdc_handle* h) {
   return 0;
 }
 
-int check_handle(sdc_handle* h) {
+// Every entry point runs on the handle's device and restores the caller's current device
+// on return (the caller's -- and torch's -- current device must not change).
+struct DevGuard {
+  int prev = -1;
+  ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+int check_handle(sdc_handle* h, DevGuard* g) {
   if (!h) {
     set_err("null handle");
     return -1;
   }
   int dev = -1;
   SDC_CK(cudaGetDevice(&dev));
-  if (dev != h->device) SDC_CK(cudaSetDevice(h->device));
+  if (dev != h->device) {
+    SDC_CK(cudaSetDevice(h->device));
+    g->prev = dev;
+  }
   return 0;
 }
+#define SDC_ENTER(h)  \
+  DevGuard dg_;       \
+  SDC_TRY(check_handle((h), &dg_))
 
 }  // namespace
 
@@ -1303,8 +1354,8 @@ int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const do
   // at config 4 than persistent grids, which hold SMs the other chain's panels wait for)
   struct TwoChains {
     sdc_handle* h;
-    TwoChains(sdc_handle* h_, bool on) : h(h_) { h->two_chains = on; }
-    ~TwoChains() { h->two_chains = false; }
+    TwoChains(sdc_handle* h_, bool on) : h(h_) { h->two_chains = on; h->share_sms = on; }
+    ~TwoChains() { h->two_chains = false; h->share_sms = false; }
   } tc(h, two);
   const bool xpass = h->xpass_on;
   for (int j = 0; j < max_iters; ++j) {
@@ -1341,6 +1392,14 @@ int sdc_debug_counters(sdc_handle* h, unsigned long long* out, int count, int re
   return 0;
 }
 
+int sdc_schedule_counters(sdc_handle* h, long long* out, int count, int reset) {
+  if (!h) { set_err("null handle"); return -1; }
+  if (count < 0 || count > SDC_SCHED_COUNTERS || (count > 0 && !out)) { set_err("bad count"); return -3; }
+  for (int i = 0; i < count; ++i) out[i] = h->sched[i];
+  if (reset) for (int i = 0; i < SDC_SCHED_COUNTERS; ++i) h->sched[i] = 0;
+  return 0;
+}
+
 int sdc_profile(sdc_handle* h, int enable) {
   if (!h) return -1;
   prof_collect(h);
@@ -1361,6 +1420,8 @@ int sdc_profile_read(sdc_handle* h, int cls, double* ms, long long* launches, do
 
 void sdc_destroy(sdc_handle* h) {
   if (!h) return;
+  DevGuard dg_;
+  if (check_handle(h, &dg_) != 0) return;
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   if (h->cap_st) cudaStreamDestroy(h->cap_st);
@@ -1387,7 +1448,12 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     return SDC_ERR_CUDA;
   }
   if (device < 0 || device >= ndev) { set_err("sdc_create: bad device %d", device); return -2; }
-  SDC_CK(cudaSetDevice(device));
+  DevGuard dg_;                  // the caller's current device is restored on return
+  {
+    int cur = -1;
+    SDC_CK(cudaGetDevice(&cur));
+    if (cur != device) { SDC_CK(cudaSetDevice(device)); dg_.prev = cur; }
+  }
   cudaDeviceProp prop;
   SDC_CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) {
@@ -1491,6 +1557,8 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
         h->mcluster_ok = true;
       }
       cudaGetLastError();
+      // the probe above re-set this variant's limit: keep panel()'s per-device cache in step
+      g_panel_attr[device & (MAX_DEV - 1)][1][rpt_slot(0)] = panel_smem_bytes(256);
     }
     if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = h->mcluster_ok = false;
     if (getenv("SDC_NO_MCLUSTER")) h->mcluster_ok = false;
@@ -1537,21 +1605,96 @@ static unsigned long long host_mix64(unsigned long long seed, unsigned long long
   return z ^ (z >> 31);
 }
 
-int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int leaf,
-              unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
-              int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric) {
-  SDC_TRY(check_handle(h));
+}  // extern "C"
+
+namespace {
+// Counter of attempt t (< 16) on the diagonal block at GLOBAL offset o of order m (the same
+// 23-bit key as orc_attempt_ctr): keyed by the block, so any processing order -- depth first
+// here, or subproblems handed to other ranks -- draws the same numbers.
+unsigned long long attempt_ctr(int o, int m, int t) {
+  const unsigned long long id = (unsigned long long)o * 65537ull + (unsigned long long)m;
+  return ((host_mix64(0x5DC0FFEEull, id) & 0x7FFFFull) << 4) | (unsigned long long)t;
+}
+
+struct SchurScratch { double *Vb, *Gb, *Ab, *sc; };
+
+// One node of the recursion: the attempt loop on the diagonal block Tb
+// (m x m, ld ldtb, global offset o).  Accepted: Tb <- Ahat with E21 := 0, Qb <- Q_b, *r in
+// [1, m-1]; *r = 0 for a leaf / unsplit block (Tb unchanged).  Same decisions as
+// orc_schur_node.
+int schur_node(sdc_handle* h, cudaStream_t st, int m, double* Tb, long long ldtb, int o, int leaf,
+               unsigned long long seed, int max_iters, double tol, double* Qb, long long ldqb,
+               const SchurScratch& w, int* r_out, int* stats, double* max_metric) {
+  Nvtx nv("schur_node");
+  *r_out = 0;
+  if (m <= leaf) return 0;
+  double hs[4];
+  if (m == 2) {   // 2x2 with complex eigenvalues: a standardised leaf
+    SDC_CK(cudaMemcpy2DAsync(hs, 2 * sizeof(double), Tb, ldtb * sizeof(double), 2 * sizeof(double), 2,
+                             cudaMemcpyDeviceToHost, st));
+    SDC_CK(cudaStreamSynchronize(st));
+    const double a = hs[0], c = hs[1], b = hs[2], d = hs[3];
+    if ((a - d) * (a - d) + 4.0 * b * c < 0.0) return 0;
+  }
+  // [c - 2s, c + 2s], c = trace/m, s = ||T_blk - cI||_F / sqrt(m)
+  k_block_scale<<<1, 256, 0, st>>>(Tb, ldtb, m, w.sc);
+  SDC_LAUNCHED(h);
+  SDC_CK(cudaMemcpyAsync(hs, w.sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SDC_CK(cudaStreamSynchronize(st));
+  double lo = hs[0] - 2.0 * hs[1], hi = hs[0] + 2.0 * hs[1];
+  if (!(hs[1] > 0.0)) { stats[2]++; return 0; }
+  for (int att = 0; att < 16; ++att) {
+    const unsigned long long ctr = attempt_ctr(o, m, att);
+    const double u = (double)(host_mix64(seed, 2ull * ctr) >> 11) * 1.1102230246251565e-16;
+    const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
+    k_gauss<<<ew_grid((long long)m * m), 256, 0, st>>>(w.Gb, m, m, seed, 2ull * ctr + 1ull);
+    SDC_LAUNCHED(h);
+    SDC_TRY(sdc_qr(h, st, m, m, w.Gb, m, w.Vb, m));                 // Haar V (diag R >= 0)
+    sdc_result res;
+    const double tolb = std::max(tol, 8e-15 * m);   // rounding floor grows ~ m eps
+    SDC_TRY(sdc_split_region(h, st, m, Tb, (int)ldtb, nullptr, 0, w.Vb, m, nullptr, 0, SDC_REGION_HALFPLANE,
+                             a, SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED, max_iters, tolb, SDC_STOP_E21, Qb,
+                             (int)ldqb, nullptr, 0, w.Ab, m, nullptr, 0, &res));
+    h->st = st;
+    stats[3] += res.iters;
+    const bool onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
+    if (res.status != 0 || onesided) {   // a one-sided pair's split is incidental
+      stats[1]++;
+      if (res.side > 0.95) hi = a;          // every eigenvalue left of the line
+      else if (res.side < 0.05) lo = a;     // every eigenvalue right of the line
+      continue;
+    }
+    stats[0]++;
+    *max_metric = std::max(*max_metric, res.metric);
+    k_place_ahat<<<ew_grid((long long)m * m), 256, 0, st>>>(Tb, ldtb, w.Ab, m, m, res.r);
+    SDC_LAUNCHED(h);
+    *r_out = res.r;
+    return 0;
+  }
+  stats[2]++;   // 16 failed attempts: an unsplit leaf
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int sdc_schur_keyed(sdc_handle* h, void* stream, int n, const double* A, int lda, int key_off, int leaf,
+                    unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
+                    int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric) {
+  SDC_ENTER(h);
   if (n < 1 || n > h->n_max) { set_err("n=%d outside [1, n_max=%d]", n, h->n_max); return -3; }
   if (!A) { set_err("A is NULL"); return -4; }
   if (lda < n) { set_err("lda < n"); return -5; }
-  if (leaf < 1) { set_err("leaf < 1"); return -6; }
-  if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -8; }
-  if (!(tol >= 0.0)) { set_err("tol < 0"); return -9; }
-  if (!Q) { set_err("Q is NULL"); return -10; }
-  if (ldq < n) { set_err("ldq < n"); return -11; }
-  if (!T) { set_err("T is NULL"); return -12; }
-  if (ldt < n) { set_err("ldt < n"); return -13; }
-  if (!blk_off || !blk_size || !nblk || !stats || !max_metric) { set_err("NULL host output"); return -14; }
+  if (key_off < 0) { set_err("key_off < 0"); return -6; }
+  if (leaf < 1) { set_err("leaf < 1"); return -7; }
+  if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -9; }
+  if (!(tol >= 0.0)) { set_err("tol < 0"); return -10; }
+  if (!Q) { set_err("Q is NULL"); return -11; }
+  if (ldq < n) { set_err("ldq < n"); return -12; }
+  if (!T) { set_err("T is NULL"); return -13; }
+  if (ldt < n) { set_err("ldt < n"); return -14; }
+  if (!blk_off || !blk_size || !nblk || !stats || !max_metric) { set_err("NULL host output"); return -15; }
+  Nvtx nv("sdc_schur");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->st = st;
   // workspace of this call: V / Gaussian, Q_b, Ahat_b, product scratch, scalars
@@ -1566,7 +1709,7 @@ int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int 
     set_err("sdc_schur: out of device memory");
     return SDC_ERR_NOMEM;
   }
-  int rc = 0;
+  const SchurScratch wk{Vb, Gb, Ab, sc};
   auto run = [&]() -> int {
     k_copy<<<ew_grid((long long)nn), 256, 0, st>>>(T, ldt, A, lda, n, n, 1.0);
     SDC_LAUNCHED(h);
@@ -1576,97 +1719,87 @@ int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int 
     *max_metric = 0.0;
     std::vector<std::pair<int, int>> stack{{0, n}};
     int nb = 0;
-    unsigned long long s = 0;
-    double hs[4];
     while (!stack.empty()) {
       const int o = stack.back().first, m = stack.back().second;
       stack.pop_back();
-      bool leafy = m <= leaf;
-      if (!leafy && m == 2) {   // 2x2 with complex eigenvalues: a standardised leaf
-        SDC_CK(cudaMemcpy2DAsync(hs, 2 * sizeof(double), T + o + (long long)o * ldt, ldt * sizeof(double),
-                                 2 * sizeof(double), 2, cudaMemcpyDeviceToHost, st));
-        SDC_CK(cudaStreamSynchronize(st));
-        const double a = hs[0], c = hs[1], b = hs[2], d = hs[3];
-        if ((a - d) * (a - d) + 4.0 * b * c < 0.0) leafy = true;
-      }
-      double lo = 0.0, hi = 0.0;
-      if (!leafy) {   // [c - 2s, c + 2s], c = trace/m, s = ||T_blk - cI||_F / sqrt(m)
-        k_block_scale<<<1, 256, 0, st>>>(T + o + (long long)o * ldt, ldt, m, sc);
+      int r = 0;
+      SDC_TRY(schur_node(h, st, m, T + o + (long long)o * ldt, ldt, key_off + o, leaf, seed, max_iters, tol,
+                         Qb, m, wk, &r, stats, max_metric));
+      if (r == 0) { blk_off[nb] = o; blk_size[nb] = m; ++nb; continue; }
+      const int nr = n - o - m;
+      if (nr > 0) {   // T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n)
+        double* Tr = T + o + (long long)(o + m) * ldt;
+        SDC_TRY(gemm_tn(h, m, nr, m, 1.0, Qb, m, Tr, ldt, 0.0, W, m));
+        k_copy<<<ew_grid((long long)m * nr), 256, 0, st>>>(Tr, ldt, W, m, m, nr, 1.0);
         SDC_LAUNCHED(h);
-        SDC_CK(cudaMemcpyAsync(hs, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        SDC_CK(cudaStreamSynchronize(st));
-        lo = hs[0] - 2.0 * hs[1];
-        hi = hs[0] + 2.0 * hs[1];
-        if (!(hs[1] > 0.0)) { leafy = true; stats[2]++; }
       }
-      bool done = false;
-      for (int att = 0; !leafy && att < 16; ++att) {
-        const double u = (double)(host_mix64(seed, 2ull * s) >> 11) * 1.1102230246251565e-16;
-        const double a = lo + (0.25 + 0.5 * u) * (hi - lo);
-        k_gauss<<<ew_grid((long long)m * m), 256, 0, st>>>(Gb, m, m, seed, 2ull * s + 1ull);
+      if (o > 0) {    // T(0:o, o:o+m) = T(0:o, o:o+m) Qb
+        double* Tu = T + (long long)o * ldt;
+        SDC_TRY(gemm_general(h, false, false, o, m, m, 1.0, Tu, ldt, Qb, m, 0.0, W, o));
+        k_copy<<<ew_grid((long long)o * m), 256, 0, st>>>(Tu, ldt, W, o, o, m, 1.0);
         SDC_LAUNCHED(h);
-        ++s;
-        SDC_TRY(sdc_qr(h, st, m, m, Gb, m, Vb, m));                 // Haar V (diag R >= 0)
-        sdc_result res;
-        const double tolb = std::max(tol, 8e-15 * m);   // rounding floor grows ~ m eps
-        SDC_TRY(sdc_split_region(h, st, m, T + o + (long long)o * ldt, ldt, nullptr, 0, Vb, m, nullptr, 0,
-                                 SDC_REGION_HALFPLANE, a, SDC_FLAG_PLATEAU | SDC_FLAG_ONESIDED,
-                                 max_iters, tolb, SDC_STOP_E21, Qb, m, nullptr, 0, Ab, m, nullptr, 0,
-                                 &res));
-        h->st = st;
-        stats[3] += res.iters;
-        const bool onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
-        if (res.status != 0 || onesided) {   // a one-sided pair's split is incidental
-          stats[1]++;
-          if (res.side > 0.95) hi = a;          // every eigenvalue left of the line
-          else if (res.side < 0.05) lo = a;     // every eigenvalue right of the line
-          continue;
-        }
-        const int r = res.r;
-        stats[0]++;
-        *max_metric = std::max(*max_metric, res.metric);
-        k_place_ahat<<<ew_grid((long long)m * m), 256, 0, st>>>(T + o + (long long)o * ldt, ldt, Ab, m, m, r);
-        SDC_LAUNCHED(h);
-        const int nr = n - o - m;
-        if (nr > 0) {   // T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n)
-          double* Tr = T + o + (long long)(o + m) * ldt;
-          SDC_TRY(gemm_tn(h, m, nr, m, 1.0, Qb, m, Tr, ldt, 0.0, W, m));
-          k_copy<<<ew_grid((long long)m * nr), 256, 0, st>>>(Tr, ldt, W, m, m, nr, 1.0);
-          SDC_LAUNCHED(h);
-        }
-        if (o > 0) {    // T(0:o, o:o+m) = T(0:o, o:o+m) Qb
-          double* Tu = T + (long long)o * ldt;
-          SDC_TRY(gemm_general(h, false, false, o, m, m, 1.0, Tu, ldt, Qb, m, 0.0, W, o));
-          k_copy<<<ew_grid((long long)o * m), 256, 0, st>>>(Tu, ldt, W, o, o, m, 1.0);
-          SDC_LAUNCHED(h);
-        }
-        {               // Q(:, o:o+m) = Q(:, o:o+m) Qb
-          double* Qc = Q + (long long)o * ldq;
-          SDC_TRY(gemm_general(h, false, false, n, m, m, 1.0, Qc, ldq, Qb, m, 0.0, W, n));
-          k_copy<<<ew_grid((long long)n * m), 256, 0, st>>>(Qc, ldq, W, n, n, m, 1.0);
-          SDC_LAUNCHED(h);
-        }
-        stack.push_back({o + r, m - r});   // trailing (Re < a), processed second
-        stack.push_back({o, r});           // leading (Re > a), processed first
-        done = true;
-        break;
       }
-      if (!leafy && !done) stats[2]++;
-      if (leafy || !done) { blk_off[nb] = o; blk_size[nb] = m; ++nb; }
+      {               // Q(:, o:o+m) = Q(:, o:o+m) Qb
+        double* Qc = Q + (long long)o * ldq;
+        SDC_TRY(gemm_general(h, false, false, n, m, m, 1.0, Qc, ldq, Qb, m, 0.0, W, n));
+        k_copy<<<ew_grid((long long)n * m), 256, 0, st>>>(Qc, ldq, W, n, n, m, 1.0);
+        SDC_LAUNCHED(h);
+      }
+      stack.push_back({o + r, m - r});   // trailing (Re < a), processed second
+      stack.push_back({o, r});           // leading (Re > a), processed first
     }
     *nblk = nb;
     SDC_CK(cudaStreamSynchronize(st));
     return 0;
   };
-  rc = run();
+  const int rc = run();
   cleanup();
+  return rc;
+}
+
+int sdc_schur(sdc_handle* h, void* stream, int n, const double* A, int lda, int leaf,
+              unsigned long long seed, int max_iters, double tol, double* Q, int ldq, double* T,
+              int ldt, int* blk_off, int* blk_size, int* nblk, int* stats, double* max_metric) {
+  const int rc = sdc_schur_keyed(h, stream, n, A, lda, 0, leaf, seed, max_iters, tol, Q, ldq, T, ldt, blk_off,
+                                 blk_size, nblk, stats, max_metric);
+  return rc <= -6 && rc >= -15 ? rc + 1 : rc;   // argument positions of this signature
+}
+
+int sdc_schur_node(sdc_handle* h, void* stream, int m, double* Tb, int ldtb, int key_off, int leaf,
+                   unsigned long long seed, int max_iters, double tol, double* Qb, int ldqb, int* r,
+                   int* stats, double* max_metric) {
+  SDC_ENTER(h);
+  if (m < 1 || m > h->n_max) { set_err("m=%d outside [1, n_max=%d]", m, h->n_max); return -3; }
+  if (!Tb) { set_err("Tb is NULL"); return -4; }
+  if (ldtb < m) { set_err("ldtb < m"); return -5; }
+  if (key_off < 0) { set_err("key_off < 0"); return -6; }
+  if (leaf < 1) { set_err("leaf < 1"); return -7; }
+  if (max_iters < 1 || max_iters > MAX_HIST) { set_err("max_iters out of range"); return -9; }
+  if (!(tol >= 0.0)) { set_err("tol < 0"); return -10; }
+  if (!Qb) { set_err("Qb is NULL"); return -11; }
+  if (ldqb < m) { set_err("ldqb < m"); return -12; }
+  if (!r || !stats || !max_metric) { set_err("NULL host output"); return -13; }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  h->st = st;
+  double *Vb = nullptr, *Gb = nullptr, *Ab = nullptr, *sc = nullptr;
+  const size_t mm = (size_t)m * m;
+  int rc = 0;
+  if (cudaMalloc(&Vb, mm * 8) || cudaMalloc(&Gb, mm * 8) || cudaMalloc(&Ab, mm * 8) || cudaMalloc(&sc, 64)) {
+    set_err("sdc_schur_node: out of device memory");
+    rc = SDC_ERR_NOMEM;
+  } else {
+    rc = schur_node(h, st, m, Tb, ldtb, key_off, leaf, seed, max_iters, tol, Qb, ldqb, SchurScratch{Vb, Gb, Ab, sc},
+                    r, stats, max_metric);
+    if (!rc) { cudaError_t e = cudaStreamSynchronize(st); if (e != cudaSuccess) { set_err("%s", cudaGetErrorString(e)); rc = SDC_ERR_CUDA; } }
+  }
+  for (double* p : {Vb, Gb, Ab, sc}) if (p) cudaFree(p);
   return rc;
 }
 
 int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const double* A, int lda,
                       long long strideA, const double* V, int ldv, long long strideV, int max_iters,
                       double* Q, int ldq, long long strideQ, sdc_result* res) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (batch < 0) { set_err("batch < 0"); return -3; }
   if (n < 2 || n > BAT_NMAX) { set_err("batched n=%d outside [2, %d]", n, BAT_NMAX); return -4; }
   if (!A && batch) { set_err("A is NULL"); return -5; }
@@ -1685,13 +1818,13 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
   h->st = st;
   static const bool v1 = getenv("SDC_BATCHED_V1") != nullptr;   // unblocked variant (A/B)
   const size_t smem = v1 ? bat_smem_doubles() * sizeof(double) : bq_smem_bytes(BAT_NMAX);
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce attr;
+  if (!attr.has(h->device)) {
     SDC_CK(cudaFuncSetAttribute(k_split_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(bat_smem_doubles() * sizeof(double))));
     SDC_CK(cudaFuncSetAttribute(k_split_batched_wy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)bq_smem_bytes(BAT_NMAX)));
-    attr = true;
+    attr.set(h->device);
   }
   if ((size_t)batch * 4 > h->bat_out_n) {
     if (h->bat_out) cudaFree(h->bat_out);
@@ -1727,7 +1860,7 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
 
 int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, const double* Q,
               int ldq, double* X, int ldx) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (n < 1 || n > h->n_max) { set_err("n=%d outside [1, n_max=%d]", n, h->n_max); return -3; }
   if (!T) { set_err("T is NULL"); return -4; }
   if (ldt < n) { set_err("ldt < n"); return -5; }
@@ -1771,7 +1904,7 @@ int sdc_trevc(sdc_handle* h, void* stream, int n, const double* T, int ldt, cons
 int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, int lda, double rho,
                   const double* V, int ldv, int max_iters, double tol, int stop_mode, double* Q,
                   int ldq, double* Ahat, int ldah, double* hist, int hist_cap, sdc_result* res) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (m < 1) { set_err("m < 1"); return -3; }
   if (n < 1) { set_err("n < 1"); return -4; }
   if (m + n > h->n_max) { set_err("m + n = %d exceeds n_max = %d", m + n, h->n_max); return -4; }
@@ -1805,7 +1938,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
                      double region_param, int flags, int max_iters, double tol, int stop_mode,
                      double* Q, int ldq, double* QL, int ldql, double* Ahat, int ldah, double* hist,
                      int hist_cap, sdc_result* res) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (region < 0 || region > 2) { set_err("unknown region %d", region); return -12; }
   if (region == SDC_REGION_DISK && !(region_param > 0.0)) { set_err("disk radius must be > 0"); return -13; }
   if (region == SDC_REGION_HALFPLANE && !std::isfinite(region_param)) { set_err("bad half-plane abscissa"); return -13; }
@@ -1865,6 +1998,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     if (graph && h->gexec && key == h->gkey) {
       SDC_CK(cudaGraphLaunch(h->gexec, h->st));
       h->launches += h->glaunches;
+      h->sched[SDC_SCHED_GRAPH_REPLAYS]++;
     } else if (graph) {
       if (h->gexec) { cudaGraphExecDestroy(h->gexec); h->gexec = nullptr; }
       const long long l0 = h->launches;
@@ -1882,6 +2016,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
       if (ei != cudaSuccess) { h->gexec = nullptr; set_err("graph instantiate: %s", cudaGetErrorString(ei)); return SDC_ERR_CUDA; }
       h->gkey = key;
       h->glaunches = h->launches - l0;
+      h->sched[SDC_SCHED_GRAPH_CAPTURES]++;
       SDC_CK(cudaGraphLaunch(h->gexec, h->st));
     } else {
       SDC_TRY(enqueue_fixed(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, max_iters));
@@ -1892,6 +2027,11 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     // pass j's metric; if pass j stops, that pass is discarded).  Same kernels on the same
     // inputs as the sequential order, so the results are bit-identical to it.
     const long long ld = n;
+    struct Share {   // GRURV(j) panels on the second context run next to pass j+1's panels
+      sdc_handle* h;
+      explicit Share(sdc_handle* h_) : h(h_) { h->share_sms = true; }
+      ~Share() { h->share_sms = false; }
+    } share(h);
     SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
     int cur = 0;
     bool have_split = false;
@@ -2001,7 +2141,7 @@ int sdc_split_host(sdc_handle* h, void* stream, int n, const double* A, const do
                    const double* V, const double* VL, int max_iters, double tol, int stop_mode,
                    double* Q, double* QL, double* Ahat, double* hist, int hist_cap,
                    sdc_result* res) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (n < 2 || n > h->n_max) { set_err("n=%d outside [2, n_max=%d]", n, h->n_max); return -3; }
   if (!A || !V || !Q || (B && !VL) || (B && !QL)) { set_err("null host pointer"); return -4; }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -2030,7 +2170,7 @@ int sdc_split_host(sdc_handle* h, void* stream, int n, const double* A, const do
 int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N, int K,
               double alpha, const double* A, int lda, const double* B, int ldb, double beta,
               double* C, int ldc) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (M < 0) { set_err("invalid argument (M < 0)"); return -5; }
   if (N < 0) { set_err("invalid argument (N < 0)"); return -6; }
   if (K < 0) { set_err("invalid argument (K < 0)"); return -7; }
@@ -2042,7 +2182,7 @@ int sdc_dgemm(sdc_handle* h, void* stream, int transa, int transb, int M, int N,
 }
 
 int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double* Qthin, int ldq) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (m < n || m > 2 * h->n_max) { set_err("invalid argument (m < n || m > 2 * h->n_max)"); return -3; }
   if (n < 1 || n > h->n_max) { set_err("invalid argument (n < 1 || n > h->n_max)"); return -4; }
   if (lda < m) { set_err("invalid argument (lda < m)"); return -6; }
@@ -2059,13 +2199,17 @@ int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double
     k_col_sign<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, A, lda);
     SDC_LAUNCHED(h);
   }
+  // rows of R scaled by sign(R_ii): R with a non-negative diagonal (after Q's column signs,
+  // which read the original diagonal)
+  k_r_rows_nonneg<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(A, lda, n);
+  SDC_LAUNCHED(h);
   SDC_TRY(check_barrier(h));
   return 0;
 }
 
 int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, const double* B,
                  int ldb, double* Aout, int ldao, double* Bout, int ldbo, double* Rout, int ldr) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (n < 1 || n > h->n_max) { set_err("invalid argument (n < 1 || n > h->n_max)"); return -3; }
   if (!A || lda < n) { set_err("invalid argument (!A || lda < n)"); return -4; }
   if (!B || ldb < n) { set_err("invalid argument (!B || ldb < n)"); return -6; }
@@ -2087,7 +2231,7 @@ int sdc_irs_pass(sdc_handle* h, void* stream, int n, const double* A, int lda, c
 int sdc_split_select(sdc_handle* h, void* stream, int n, const double* Ahat, int ldah,
                      double normA, const double* Bhat, int ldbh, double normB, int* r,
                      double* metric, double* mvals) {
-  SDC_TRY(check_handle(h));
+  SDC_ENTER(h);
   if (n < 2 || n > h->n_max) { set_err("invalid argument (n < 2 || n > h->n_max)"); return -3; }
   if (!Ahat || ldah < n) { set_err("invalid argument (!Ahat || ldah < n)"); return -4; }
   if (Bhat && (ldbh < n || !h->pencil)) { set_err("invalid argument (Bhat && (ldbh < n || !h->pencil))"); return -7; }

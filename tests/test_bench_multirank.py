@@ -50,3 +50,13 @@ def test_single_rank_passthrough():
     import bench
     assert bench.max_over_ranks(12.5, 1) == 12.5
     assert bench.replica_throughput(500.0, 1) == 2.0
+
+
+def test_gpus_must_match_world_size():
+    # --gpus N under a launcher that started a different number of ranks is refused (the
+    # line would otherwise report N GPUs for a run of WORLD_SIZE replicas: VERDICT r01 weak 9)
+    import subprocess
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                        "reference"], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE=1" in r.stderr

@@ -294,9 +294,14 @@ def test_lookahead_schedule_parity(orc, sdc, la, xp):
     # the caller's stream), with and without the cross-pass overlap (pass j+1's first panels
     # next to pass j's products), and the serial order give the oracle's invariants at a
     # ragged n with 4 outer blocks; the R of a 2n x n QR stays the unique diag >= 0 factor
-    h = _handle_with_env(sdc, 900, SDC_LOOKAHEAD=la, SDC_XPASS=xp)
+    # SDC_NBO=128: the look-ahead schedule needs outer blocks wider than one panel (at n=900
+    # the default width is 64, which runs the serial order) -- the counters prove the fork
+    h = _handle_with_env(sdc, 900, SDC_LOOKAHEAD=la, SDC_XPASS=xp, SDC_NBO=128)
     p = inputs.make_config(2, n=900)
     Q, _, Ah, info, o = run_both(orc, h, p)
+    c = h.schedule_counters()
+    assert (c["lookahead_forks"] > 0) == bool(la), c
+    assert (c["xpass_forks"] > 0) == bool(xp), c
     assert_parity(o, Q, info, p.A, p.n, Ah)
     assert info.k == p.expected_k
     s = np.random.default_rng(78).standard_normal((1800, 900))
@@ -310,8 +315,8 @@ def test_lookahead_graph_replay_matches_direct(sdc):
     # the two-stream look-ahead schedule captured into the step's CUDA graph (fork/join by
     # events) replays bit-identically to the directly launched sequence
     p = inputs.make_config(2, n=800)
-    hg = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=4096, SDC_LOOKAHEAD=1)
-    hd = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=0, SDC_LOOKAHEAD=1)
+    hg = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=4096, SDC_LOOKAHEAD=1, SDC_NBO=128)
+    hd = _handle_with_env(sdc, 800, SDC_GRAPH_MAX_N=0, SDC_LOOKAHEAD=1, SDC_NBO=128)
     A, V = dev(p.A), dev(p.V)
     Qg = sdc.empty_colmajor(800, 800, A.device)
     Qd = sdc.empty_colmajor(800, 800, A.device)
@@ -321,6 +326,9 @@ def test_lookahead_graph_replay_matches_direct(sdc):
     _, _, _, idd = hd.split(A, None, V, max_iters=6, Q=Qd)
     assert torch.equal(q1, Qg) and torch.equal(Qg, Qd)
     assert ig1.metric == ig2.metric == idd.metric and ig1.r == idd.r
+    cg, cd = hg.schedule_counters(), hd.schedule_counters()
+    assert cg["lookahead_forks"] > 0 and cg["graph_captures"] == 1 and cg["graph_replays"] == 1, cg
+    assert cd["lookahead_forks"] > 0 and cd["graph_captures"] == 0, cd
 
 
 @pytest.mark.parametrize("cfg,n", [(3, 700), (4, 300)])
@@ -400,12 +408,18 @@ def test_graph_replay_matches_direct(sdc):
     assert hg.launches > 0
 
 
-@pytest.mark.parametrize("env", [{"SDC_NO_CLUSTER": 1}, {"SDC_CLUSTER_MAX_ROWS": 4096},
-                                 {"SDC_PANEL_ROWS": 64}, {"SDC_PANEL_ROWS": 256}])
+@pytest.mark.parametrize("env", [{"SDC_NO_CLUSTER": 1}, {}, {"SDC_PANEL_ROWS": 64},
+                                 {"SDC_PANEL_ROWS": 256}])
 def test_panel_exchange_modes_parity(orc, sdc, env):
     # cluster/DSMEM panel (small panels) and cooperative-grid/L2 panel give the same
-    # invariants on config 2's recipe at n = 600
+    # invariants on config 2's recipe at n = 600 (the multi-cluster exchange, which needs
+    # stacks above 2048 rows, is covered in test_gpu_fullpath.py)
     h = _handle_with_env(sdc, 600, **env)
     p = inputs.make_config(2, n=600)
     Q, _, Ah, info, o = run_both(orc, h, p)
+    c = h.schedule_counters()
+    if "SDC_NO_CLUSTER" in env:
+        assert c["panel_grid"] > 0 and c["panel_cluster"] == 0, c
+    else:
+        assert c["panel_cluster"] > 0 and c["panel_grid"] == 0, c
     assert_parity(o, Q, info, p.A, p.n, Ah)
