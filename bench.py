@@ -328,8 +328,27 @@ def run_schur(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
 
+    kw = dict(leaf=leaf, seed=5, max_iters=60, tol=1e-13)
+    if world > 1:
+        # one decomposition across the ranks: the smaller subproblem of each split goes to an
+        # idle rank (paper_1011_3077_b200/parallel_schur.py), NCCL send/recv
+        from paper_1011_3077_b200 import parallel_schur as ps
+
+        def one():
+            be = ps.GpuBackend(h, **kw)
+            out = ps.schur(be, dist, rank, world, A if rank == 0 else None)
+            if out is None:
+                return None, None
+            Qd, Td, blocks, st_ = out
+            c = st_.counts
+            return blocks, {"splits": int(c[0]), "failed_attempts": int(c[1]), "unsplit": int(c[2]),
+                            "passes": int(c[3]), "max_metric": st_.max_metric}, Qd, Td
+    else:
+        def one():
+            _, _, blocks, info = h.schur(A, Q=Q, T=T, **kw)
+            return blocks, info, Q, T
     for _ in range(args.warmup):
-        h.schur(A, leaf=leaf, seed=5, Q=Q, T=T)
+        one()
     barrier()
     st = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -339,7 +358,7 @@ def run_schur(args, rank, world, local):
         barrier()
         e0.record(st)
         for _ in range(args.steps):
-            _, _, blocks, info = h.schur(A, leaf=leaf, seed=5, Q=Q, T=T)
+            res = one()
         e1.record(st)
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
@@ -351,17 +370,21 @@ def run_schur(args, rank, world, local):
         if world > 1:
             dist.destroy_process_group()
         return 0
+    blocks, info, Q, T = res
     # accuracy of this run (test-side torch checks, outside the timed region)
     resid = float(torch.linalg.matrix_norm(Q @ T @ Q.T - A, 1) / torch.linalg.matrix_norm(A, 1))
     achieved = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
     clocks = clk.summary()
     line = {"metric": "block Schur decompositions/s by recursive divide-and-conquer (f2)",
-            "value": 1e3 / ms * world, "unit": "decompositions/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "value": 1e3 / ms, "unit": "decompositions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg8: sdc_schur of a normal matrix with eigenvalues Re, Im ~ U[-1.5,1.5] "
                                    f"(conjugate pairs, seed 88), n={n}, leaf {leaf}, seed 5, monitor tol 1e-13",
-                       "n": n, "leaf": leaf, "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "n": n, "leaf": leaf,
+                       "parallelism": (f"recursion over {world} ranks (smaller subproblem handed off per split)"
+                                       if world > 1 else "single"),
                        "l2": "working set (5 n^2 doubles) exceeds L2; no flush needed"},
             "result": {"blocks": len(blocks), "max_block": max(m for _, m in blocks), **info,
                        "residual_1": resid},

@@ -169,8 +169,9 @@ int sdc_svd_split(sdc_handle* h, void* stream, int m, int n, const double* A, in
 
 /* Batched small-n split step: `batch` independent RNEP steps on the
  * unit disk (Alg. 5, FIXED passes), one CTA per problem with the whole step in shared
- * memory (unblocked routines in the oracle's order: dgeqr2, complement, GRURV via dgerq2 /
- * dorgr2, similarity with the original A, split selection).  2 <= n <= 64.
+ * memory (compact-WY Householder QR, complement-free IRS products, GRURV with the RQ as a
+ * reversed QR, similarity with the original A, split selection; every O(n^3) product on
+ * DMMA from shared memory).  2 <= n <= 64.
  *  1 h, 2 stream
  *  3 batch      >= 0 problems
  *  4 n          order of every problem
@@ -330,9 +331,13 @@ enum { SDC_SCHED_LOOKAHEAD_FORKS = 0,  /* look-ahead QR schedules forked to the 
        SDC_SCHED_GRAPH_REPLAYS = 7,    /* fixed-mode steps replayed from the graph              */
        SDC_SCHED_PANEL_MCLUSTER_CAPPED = 8, /* multi-cluster panels limited to half the
                                           resident clusters (two contexts share the SMs)   */
-       SDC_SCHED_COUNTERS = 9 };
+       SDC_SCHED_PANEL_CQR_TRIED = 9,  /* panels launched with the CholeskyQR2 path first     */
+       SDC_SCHED_PANEL_CQR_DONE = 10,  /* ... factored by it (device count; reading it syncs)  */
+       SDC_SCHED_PANEL_CQR_FALLBACK = 11, /* ... that fell back to the Householder loop      */
+       SDC_SCHED_COUNTERS = 12 };
 /* Copies `count` (<= SDC_SCHED_COUNTERS) counters to the HOST array out; reset != 0 zeroes
- * them.  Returns 0, -1 (null handle) or -3 (bad count). */
+ * them.  count > SDC_SCHED_PANEL_CQR_DONE synchronises the device (device-side counters).
+ * Returns 0, -1 (null handle), -3 (bad count) or -100. */
 int sdc_schedule_counters(sdc_handle* h, long long* out, int count, int reset);
 
 /* Text of the last error on this thread ("" if none). */

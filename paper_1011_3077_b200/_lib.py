@@ -14,7 +14,8 @@ FLAG_SYMMETRIC, FLAG_PLATEAU, FLAG_ONESIDED, FLAG_QL_ORTH = 1, 2, 4, 8
 PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PROF_GEMM_OTHER = 0, 1, 2, 3, 4, 5, 6
 SPLIT_ACCEPT = 1e-8
 SCHED_NAMES = ("lookahead_forks", "xpass_forks", "ctx_forks", "panel_cluster", "panel_mcluster",
-               "panel_grid", "graph_captures", "graph_replays", "panel_mcluster_capped")
+               "panel_grid", "graph_captures", "graph_replays", "panel_mcluster_capped", "panel_cqr_tried",
+               "panel_cqr_done", "panel_cqr_fallback")
 
 
 class SdcResult(ctypes.Structure):

@@ -4,9 +4,8 @@
 //
 // For n <= 64 the large-n machinery (64-wide panels, DMMA GEMM tiles, per-column grid
 // exchanges) is all latency: a single problem keeps one SM busy for ~3 ms at n = 64.  Here
-// each CTA runs the unblocked textbook routines (the oracle's order: dgeqr2, complement,
-// dgerq2 / dorgr2 for the RQ of GRURV, plain products), every matrix in SMEM, so a launch
-// of B problems runs B/148 waves of independent CTAs: data-parallel over problems, which is
+// each CTA runs the whole step with every matrix in SMEM, so a launch of B problems runs
+// B/148 waves of independent CTAs: data-parallel over problems, which is
 // also how the batch shards across GPUs (no collective, `bench.py --config 10`).
 #pragma once
 #include "common.cuh"
@@ -16,11 +15,6 @@ namespace sdc {
 constexpr int BAT_NMAX = 64;
 constexpr int BAT_THREADS = 512;
 constexpr int BAT_WARPS = BAT_THREADS / 32;
-
-// shared memory (doubles): Aj, Bj (n x n), S, C (2n x n), X (n x n scratch), vectors
-constexpr size_t bat_smem_doubles() {
-  return 3 * (size_t)BAT_NMAX * BAT_NMAX + 4 * (size_t)BAT_NMAX * BAT_NMAX + 4 * BAT_NMAX + 2 * BAT_WARPS + 16;
-}
 
 struct BatArgs {
   const double* A; long long lda, sa;    // problem b: A + b*sa, n x n, ld lda
@@ -47,268 +41,11 @@ SDC_DEV double bat_sum(double v, double* red) {
   return t;
 }
 
-// LAPACK dlarfg (reading Q7) on alpha = *a, x = a[step], ..., nx entries:
-// scales x in place, writes beta to *a, returns tau (all threads)
-SDC_DEV double bat_larfg(int nx, double* a, const long long step, double* red) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < nx; i += BAT_THREADS) {
-    const double x = a[(long long)(i + 1) * step];
-    s += x * x;
-  }
-  const double xn2 = bat_sum(s, red);
-  if (xn2 == 0.0) return 0.0;
-  const double al = *a;
-  const double nrm = sqrt(al * al + xn2);
-  const double beta = al < 0.0 ? nrm : -nrm;
-  const double tau = (beta - al) / beta;
-  const double scal = 1.0 / (al - beta);
-  for (int i = threadIdx.x; i < nx; i += BAT_THREADS) a[(long long)(i + 1) * step] *= scal;
-  __syncthreads();
-  if (threadIdx.x == 0) *a = beta;
-  __syncthreads();
-  return tau;
-}
-
-// C(k:m, c0:c1) <- (I - tau v v^T) C, v = [1; Y(k+1:m, k)]  (columns by warps)
-SDC_DEV void bat_apply_left(int m, int k, const double* Y, int ldy, double tau, double* C, int ldc,
-                            int c0, int c1, double* wbuf) {
-  if (tau == 0.0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = c0 + warp; j < c1; j += BAT_WARPS) {
-    double w = 0.0;
-    for (int i = k + 1 + lane; i < m; i += 32) w = fma(Y[i + k * ldy], C[i + j * ldc], w);
-    w = warp_sum(w);
-    if (lane == 0) wbuf[j] = tau * (C[k + j * ldc] + w);
-  }
-  __syncthreads();
-  const int rows = m - k, cols = c1 - c0;
-  for (int e = threadIdx.x; e < rows * cols; e += BAT_THREADS) {
-    const int i = k + e % rows, j = c0 + e / rows;
-    const double w = wbuf[j];
-    C[i + j * ldc] -= (i == k) ? w : w * Y[i + k * ldy];
-  }
-  __syncthreads();
-}
-
-// dgeqr2 of the m x n Y (ld ldy) in place
-SDC_DEV void bat_geqr2(int m, int n, double* Y, int ldy, double* tau, double* red, double* wbuf) {
-  for (int k = 0; k < n; ++k) {
-    const double t = bat_larfg(m - k - 1, Y + k + k * ldy, 1, red);
-    if (threadIdx.x == 0) tau[k] = t;
-    bat_apply_left(m, k, Y, ldy, t, Y, ldy, k + 1, n, wbuf);
-  }
-  __syncthreads();
-}
-
-// out (p x q, ld ldo) = op(X) op(Y); X, Y n-inner; all in SMEM
-template <bool TX, bool TY>
-SDC_DEV void bat_gemm(int p, int q, int K, const double* X, int ldx, const double* Y, int ldy,
-                      double* out, int ldo, double alpha) {
-  for (int e = threadIdx.x; e < p * q; e += BAT_THREADS) {
-    const int i = e % p, j = e / p;
-    double s = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double x = TX ? X[k + i * ldx] : X[i + k * ldx];
-      const double y = TY ? Y[j + k * ldy] : Y[k + j * ldy];
-      s = fma(x, y, s);
-    }
-    out[i + j * ldo] = alpha * s;
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(BAT_THREADS, 1) k_split_batched(const BatArgs a) {
-  extern __shared__ __align__(16) double smb[];
-  const int n = a.n, m = 2 * n, b = blockIdx.x, tid = threadIdx.x;
-  const int NN = BAT_NMAX * BAT_NMAX;
-  double* Aj = smb;                 // n x n, ld n
-  double* Bj = Aj + NN;
-  double* X = Bj + NN;              // n x n scratch
-  double* S = X + NN;               // 2n x n, ld 2n
-  double* C = S + 2 * NN;           // 2n x n, ld 2n
-  double* tau = C + 2 * NN;
-  double* tau2 = tau + BAT_NMAX;
-  double* wbuf = tau2 + BAT_NMAX;   // BAT_NMAX
-  double* msel = wbuf + BAT_NMAX;   // BAT_NMAX
-  double* red = msel + BAT_NMAX;    // 2 * BAT_WARPS + 16
-  const double* A0 = a.A + (long long)b * a.sa;
-  const double* V0 = a.V + (long long)b * a.sv;
-
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    Aj[e] = A0[i + (long long)j * a.lda];
-    Bj[e] = i == j ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // ||A||_1, ||A||_F of the input
-  double nA = 0.0, fA;
-  {
-    double f = 0.0;
-    for (int e = tid; e < n * n; e += BAT_THREADS) f += Aj[e] * Aj[e];
-    fA = sqrt(bat_sum(f, red));
-    if (tid < n) {
-      double c = 0.0;
-      for (int i = 0; i < n; ++i) c += fabs(Aj[i + tid * n]);
-      msel[tid] = c;
-    }
-    __syncthreads();
-    for (int j = 0; j < n; ++j) nA = fmax(nA, msel[j]);
-    __syncthreads();
-  }
-
-  // ---- IRS passes (Alg. 3): [B_j; -A_j] = Q [R; 0], A <- Q12^T A, B <- Q22^T B ----------
-  for (int p = 0; p < a.passes; ++p) {
-    for (int e = tid; e < n * n; e += BAT_THREADS) {
-      const int i = e % n, j = e / n;
-      S[i + j * m] = Bj[e];
-      S[n + i + j * m] = -Aj[e];
-    }
-    __syncthreads();
-    bat_geqr2(m, n, S, m, tau, red, wbuf);
-    for (int e = tid; e < m * n; e += BAT_THREADS) {     // C = [0; I]
-      const int i = e % m, j = e / m;
-      C[e] = (i == n + j) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    for (int k = n - 1; k >= 0; --k) bat_apply_left(m, k, S, m, tau[k], C, m, 0, n, wbuf);
-    bat_gemm<true, false>(n, n, n, C, m, Aj, n, X, n, 1.0);       // Q12^T A_j
-    bat_gemm<true, false>(n, n, n, C + n, m, Bj, n, S, n, 1.0);   // Q22^T B_j (S free)
-    for (int e = tid; e < n * n; e += BAT_THREADS) { Aj[e] = X[e]; Bj[e] = S[e]; }
-    __syncthreads();
-  }
-
-  // ---- GRURV(2, A_p + B_p, A_p; -1, +1) (Alg. 1/2, oracle orc_grurv_right) ---------------
-  // X = A_p V^T
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    C[i + j * n] = V0[i + (long long)j * a.ldv];                   // V (ld n) into C
-  }
-  __syncthreads();
-  bat_gemm<false, true>(n, n, n, Aj, n, C, n, X, n, 1.0);
-  bat_geqr2(n, n, X, n, tau, red, wbuf);                          // X = U R_2
-  for (int e = tid; e < n * n; e += BAT_THREADS) S[e] = Aj[e] + Bj[e];   // S (ld n) = A_p + B_p
-  __syncthreads();
-  for (int k = 0; k < n; ++k) bat_apply_left(n, k, X, n, tau[k], S, n, 0, n, wbuf);   // U^T S
-  for (int e = tid; e < n * n; e += BAT_THREADS) {                // U <- U D_U
-    const int i = e % n;
-    if (X[i + i * n] < 0.0) S[e] = -S[e];
-  }
-  __syncthreads();
-  // dgerq2 of S (n x n, ld n): rows from n-1 down, reflector from the right on columns 0..i
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int i = n - 1; i >= 0; --i) {
-    const double t = bat_larfg(i, S + i + i * n, -(long long)n, red);
-    // bat_larfg walks a[(k+1)*step] = row i, columns i-1, i-2, ... 0: reorder-free (scaling
-    // is elementwise; the norm is a fixed-order sum over the same entries)
-    if (tid == 0) tau2[i] = t;
-    if (t != 0.0) {
-      for (int r = warp; r < i; r += BAT_WARPS) {
-        double w = 0.0;
-        for (int c = lane; c < i; c += 32) w = fma(S[r + c * n], S[i + c * n], w);
-        w = warp_sum(w);
-        if (lane == 0) wbuf[r] = t * (S[r + i * n] + w);
-      }
-      __syncthreads();
-      for (int e = tid; e < i * (i + 1); e += BAT_THREADS) {
-        const int r = e % i, c = e / i;          // c in 0..i
-        const double w = wbuf[r];
-        S[r + c * n] -= (c == i) ? w : w * S[i + c * n];
-      }
-      __syncthreads();
-    }
-  }
-  // Q_rq = H(0)...H(n-1) (H(n-1) applied first to I), rows sign-fixed; Q = Q_rq^T
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    C[e] = i == j ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int i = n - 1; i >= 0; --i) {
-    const double t = tau2[i];
-    if (t == 0.0) continue;
-    for (int j = warp; j < n; j += BAT_WARPS) {
-      double w = 0.0;
-      for (int c = lane; c < i; c += 32) w = fma(S[i + c * n], C[c + j * n], w);
-      w = warp_sum(w);
-      if (lane == 0) wbuf[j] = t * (C[i + j * n] + w);
-    }
-    __syncthreads();
-    for (int e = tid; e < (i + 1) * n; e += BAT_THREADS) {
-      const int r = e % (i + 1), j = e / (i + 1);
-      const double w = wbuf[j];
-      C[r + j * n] -= (r == i) ? w : w * S[i + r * n];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < n * n; e += BAT_THREADS) {   // X = Q = (D Q_rq)^T
-    const int i = e % n, j = e / n;
-    const double d = S[j + j * n] < 0.0 ? -1.0 : 1.0;
-    X[i + j * n] = d * C[j + i * n];
-  }
-  __syncthreads();
-
-  // ---- similarity Ahat = Q^T A Q with the original A, split selection ----------------------
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    Bj[e] = A0[i + (long long)j * a.lda];                          // original A
-  }
-  __syncthreads();
-  bat_gemm<false, false>(n, n, n, Bj, n, X, n, S, n, 1.0);        // A Q
-  bat_gemm<true, false>(n, n, n, X, n, S, n, Aj, n, 1.0);         // Q^T (A Q) = Ahat
-  // suffix column sums: C[c + r n] = sum_{i >= r} |Ahat(i, c)| for c < r
-  if (tid < n) {
-    double s = 0.0;
-    for (int r = n - 1; r >= 1; --r) {
-      s += fabs(Aj[r + tid * n]);
-      C[tid + r * n] = s;
-    }
-  }
-  __syncthreads();
-  if (tid >= 1 && tid < n) {
-    const int r = tid;
-    double ma = 0.0;
-    for (int c = 0; c < r; ++c) {
-      const double v = C[c + r * n];
-      if (v > ma || v != v) ma = v;
-    }
-    msel[r] = ma / nA;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int best = 1;
-    for (int r = 2; r <= n - 1; ++r)
-      if (msel[r] < msel[best]) best = r;
-    red[2 * BAT_WARPS] = best;
-    red[2 * BAT_WARPS + 1] = msel[best];
-  }
-  __syncthreads();
-  const int rbest = (int)red[2 * BAT_WARPS];
-  double f = 0.0, nf = 0.0;
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    const double v = Aj[e];
-    if (i >= rbest && j < rbest) f += v * v;
-    if (!(fabs(v) <= 1.79e308)) nf = 1.0;
-  }
-  const double e21f = sqrt(bat_sum(f, red));
-  const double nonfinite = bat_sum(nf, red);
-  double* Qo = a.Q + (long long)b * a.sq;
-  for (int e = tid; e < n * n; e += BAT_THREADS) {
-    const int i = e % n, j = e / n;
-    Qo[i + (long long)j * a.ldq] = X[e];
-  }
-  if (tid == 0) {
-    a.out[4 * b + 0] = rbest;
-    a.out[4 * b + 1] = red[2 * BAT_WARPS + 1];
-    a.out[4 * b + 2] = e21f / fA;
-    a.out[4 * b + 3] = nonfinite;
-  }
-}
-
 // =======================================================================================
-// Compact-WY variant (default): the same step with every O(n^3) contraction on the FP64
-// tensor cores (mma.sync m8n8k4 DMMA on shared-memory operands) and 2 CTA barriers per
-// Householder column instead of ~5:
+// Compact-WY kernel: the step with every O(n^3) contraction on the FP64 tensor cores
+// (mma.sync m8n8k4 DMMA on shared-memory operands) and 2 CTA barriers per Householder
+// column (the first, unblocked version with the oracle's dgeqr2 / complement / dgerq2 order
+// needed ~5 and ran 3.7x slower; removed in round 2):
 //   QR (bq_qr): reflector columns stay UNSCALED during the factorisation (v_k = sc_k x_k),
 //     one pass of column dot products g_j = x_k^T P(:, j) per column gives the norm, the
 //     update coefficients and the Gram entries of the compact-WY T column (PAPER.md:331's

@@ -23,7 +23,10 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "common.cuh"
+#include "cqr.cuh"
 
 namespace sdc {
 
@@ -76,6 +79,9 @@ struct PanelArgs {
   int csize;                  // cluster mode: CTAs per cluster (G / csize clusters)
   double* ll;                 // multi-cluster: flag-carrying slots, 2 x (16 + 1) x PANEL_NB x 16 B
   unsigned epoch;             // multi-cluster: flag of column k is epoch + k + 1 (unique per call)
+  double* cq;                 // CholeskyQR2 exchange slots (CQ_DOUBLES), flags epoch + 1..3
+  int use_cqr;                // try the CholeskyQR2 panel first (cqr.cuh); Householder on breakdown
+  unsigned long long* cqstat; // [0] panels factored by CholeskyQR2, [1] Householder fallbacks
 };
 constexpr size_t PANEL_LL_DOUBLES = 2 * 17 * 64 * 2;
 
@@ -141,6 +147,99 @@ SDC_DEV void panel_t_column(double* Ts, int c, const double* tot, const double* 
   if (threadIdx.x == 0) Ts[c * PANEL_NB + c] = tau;
 }
 
+// CholeskyQR2 + Householder reconstruction of the panel (cqr.cuh).  Ps holds the CTA's R
+// rows (row-major, ld PANEL_LD); scr >= CQ_SCRATCH doubles of shared memory.  Returns
+// 0: factored -- Ps rows with global index >= 64 hold Y, CTA 0's rows 0..63 hold L (strictly
+//    lower) and U; R (with D) is already in P(0:64, 0:64) upper, T and tau in a.T / a.tau;
+// 1: breakdown at the first Cholesky (Ps untouched); 2: breakdown at the second (Ps holds
+//    Q1: the caller reloads the panel).  Every CTA returns the same code.
+__device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, double* scr) {
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
+  double* Am = scr;                        // 64 x CQ_LD
+  double* Bm = Am + 64 * CQ_LD;            // 64 x CQ_LD
+  double* gd = Bm + 64 * CQ_LD;            // Cholesky column norms^2
+  double* dv = gd + 64;                    // 1 / sqrt(pivot)
+  double* r1d = dv + 64;                   // diag R1
+  double* dsg = r1d + 64;                  // D
+  double* ukk = dsg + 64;                  // U_kk
+  unsigned* err = a.bar + 1;
+  double* reg0 = a.cq;
+  double* reg1 = a.cq + CQ_REGION;
+  double* mreg = a.cq + 2 * (size_t)CQ_REGION;
+  const unsigned f1 = a.epoch + 1u, f2 = a.epoch + 2u, f3 = a.epoch + 3u;
+  const int eper = (CQ_E + G - 1) / G, e0 = min(CQ_E, cta * eper), e1 = min(CQ_E, e0 + eper);
+  // (1) G1 = P^T P (owner-reduced through L2), R1 = chol(G1)
+  cq_gram_partial(Ps, PANEL_LD, R, reg0 + 2 * (size_t)cta * CQ_E, f1);
+  cq_owner_reduce(reg0, G, e0, e1, f1, err);
+  cq_gather<true>(reg0 + 2 * (size_t)G * CQ_E, f1, Am, err);
+  __syncthreads();
+  if (!cq_chol(Am, gd, dv)) return 1;
+  // (2) Q1 = P R1^{-1} in place; keep R1 (transposed into Bm's lower part, diagonal in r1d)
+  cq_trinv_upper(Am, Bm);
+  __syncthreads();
+  cq_rows_times_upper(Ps, PANEL_LD, R, 0, Bm);
+  __syncthreads();
+  for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
+    const int i = e & 63, j = e >> 6;
+    if (i < j) Bm[j + i * CQ_LD] = Am[i + j * CQ_LD];
+    else if (i == j) r1d[i] = Am[i + i * CQ_LD];
+  }
+  __syncthreads();
+  // (3) G2 = Q1^T Q1, R2 = chol(G2)
+  cq_gram_partial(Ps, PANEL_LD, R, reg1 + 2 * (size_t)cta * CQ_E, f2);
+  cq_owner_reduce(reg1, G, e0, e1, f2, err);
+  cq_gather<true>(reg1 + 2 * (size_t)G * CQ_E, f2, Am, err);
+  __syncthreads();
+  if (!cq_chol(Am, gd, dv)) return 2;
+  if (cta == 0) {
+    // (4) Q_top = Q1(0:64,:) R2^{-1}; Q_top - D = L U; R = D R2 R1 -> P(0:64, 0:64) upper
+    cq_trsm_rows64(Ps, PANEL_LD, Am);
+    __syncthreads();
+    cq_lu_signed(Ps, PANEL_LD, dsg, ukk);
+    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
+      const int i = e & 63, j = e >> 6;
+      if (i > j) continue;
+      double acc = 0.0;
+      for (int l = i; l <= j; ++l) acc = fma(Am[i + l * CQ_LD], l == j ? r1d[j] : Bm[j + l * CQ_LD], acc);
+      a.P[(long long)i + (long long)j * a.ldp] = dsg[i] * acc;
+    }
+    __syncthreads();
+    // (5) W = U R2 (Bm upper), M = W^{-1} = R2^{-1} U^{-1} (Am), published for every CTA
+    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
+      const int i = e & 63, j = e >> 6;
+      if (i > j) continue;
+      double acc = 0.0;
+      for (int l = i; l <= j; ++l) acc = fma(Ps[i * PANEL_LD + l], Am[l + j * CQ_LD], acc);
+      Bm[i + j * CQ_LD] = acc;
+    }
+    __syncthreads();
+    cq_trinv_upper(Bm, Am);
+    __syncthreads();
+    for (int p = tid; p < CQ_E; p += PANEL_THREADS) {
+      const int j = cq_col(p), i = p - j * (j + 1) / 2;
+      cq_ll_store(mreg + 2 * (size_t)p, Am[i + j * CQ_LD], f3);
+    }
+    // (6) T = -U D L^{-T} (upper), tau = diag T
+    cq_trinv_unit_lower(Ps, PANEL_LD, Bm);
+    __syncthreads();
+    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
+      const int i = e & 63, j = e >> 6;
+      double acc = 0.0;
+      if (i <= j)
+        for (int l = i; l <= j; ++l) acc = fma(Ps[i * PANEL_LD + l] * dsg[l], Bm[j + l * CQ_LD], acc);
+      a.T[e] = -acc;                        // a.T is nb x nb = 64 x 64, column-major
+      if (i == j) a.tau[i] = -acc;
+    }
+  } else {
+    cq_gather<false>(mreg, f3, Am, err);
+  }
+  __syncthreads();
+  // (7) Y(64:m, :) = Q1 M for the rows below the panel's top 64
+  cq_rows_times_upper(Ps, PANEL_LD, R, cta == 0 ? 64 : 0, Am);
+  __syncthreads();
+  return 0;
+}
+
 // CLUSTER = false: G CTAs of a cooperative grid exchange per-CTA partials through L2 and a
 //                  grid barrier (any m; used for the tall stacks of large n).
 // CLUSTER = true : the G <= 16 CTAs form ONE thread-block cluster and exchange partials
@@ -185,6 +284,27 @@ panel_qr_kernel_t(const PanelArgs a) {
   cp_async_commit();
   cp_async_wait<0>();
   const int tcta = G - 1;                          // builds T (fewest rows: off the critical path)
+  bool cqr_done = false;
+  const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
+  unsigned long long ph[4] = {0, 0, 0, 0}, tloop = 0, tlend = 0;
+  if constexpr (CLUSTER && RPT > 0) {
+    // CholeskyQR2 + Householder reconstruction: 3 exchanges instead of one per column
+    if (a.use_cqr && nb == PANEL_NB) {
+      __syncthreads();
+      const int rc = panel_cqr(a, Ps, R, red);
+      cqr_done = rc == 0;
+      if (cta == 0 && tid == 0 && a.cqstat) atomicAdd(a.cqstat + (cqr_done ? 0 : 1), 1ull);
+      if (rc == 2) {                               // Ps holds Q1: reload the panel
+        for (int e = tid; e < R * nb; e += PANEL_THREADS) {
+          int j = e / R, r = e % R;
+          cp_async_zfill<8>(Ps + r * PANEL_LD + j, a.P + (long long)(r0 + r) + (long long)j * a.ldp, 8);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+      }
+    }
+  }
+  if (!cqr_done) {                                 // Householder column loop (fallback)
   if (cta == tcta)
     for (int e = tid; e < PANEL_NB * PANEL_NB; e += PANEL_THREADS) Ts[e] = 0.0;
   __syncthreads();
@@ -216,8 +336,7 @@ panel_qr_kernel_t(const PanelArgs a) {
   const int CS = CLUSTER ? a.csize : 1;               // CTAs per cluster
   const int NCL = CLUSTER ? G / CS : 1;               // clusters (> 1: two-level exchange)
   const int crank = cta % CS, cid = cta / CS;
-  const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
-  unsigned long long ph[4] = {0, 0, 0, 0}, t0 = 0, t1;
+  unsigned long long t0 = 0, t1;
 #ifdef SDC_PANEL_SUBPHASES   // fine-grained phase timers (tools/panel_bench.py; costs registers)
   unsigned long long sp[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tsp = 0;
 #define PSTAMP(q) if (timed) { const unsigned long long _t = clock64(); sp[q] += _t - tsp; tsp = _t; }
@@ -226,7 +345,7 @@ panel_qr_kernel_t(const PanelArgs a) {
 #define PSTAMP(q)
 #define PSTAMP0()
 #endif
-  const unsigned long long tloop = clock64();
+  tloop = clock64();
   for (int k = 0; k < nb; ++k) {
     if (timed) t0 = clock64();
     PSTAMP0();
@@ -467,7 +586,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     PSTAMP(9);
     if (timed) { t1 = clock64(); ph[3] += t1 - t0; }
   }
-  const unsigned long long tlend = clock64();
+  tlend = clock64();
   if (cta == tcta) {
     panel_t_column(Ts, nb - 1, totb + ((nb - 1) & 1) * PANEL_NB, drowb + ((nb - 1) & 1) * PANEL_NB,
                    sc, tauv);
@@ -481,6 +600,10 @@ panel_qr_kernel_t(const PanelArgs a) {
   }
   if constexpr (CLUSTER) cooperative_groups::this_cluster().sync();  // peers done reading our smem
   else __syncthreads();
+  }  // Householder column loop
+  if (cqr_done)                                   // CQR path: sc = 1 (Y stored unscaled in Ps)
+    for (int j = tid; j < PANEL_NB; j += PANEL_THREADS) sc[j] = 1.0;
+  __syncthreads();
   const unsigned long long tend = clock64();
 
   // write back: R above the diagonal, v = s_j x below it (LAPACK layout), explicit Y, Y^T
@@ -489,7 +612,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     int gr = r0 + r;
     double x = Ps[r * PANEL_LD + j];
     double v = gr > j ? sc[j] * x : x;
-    a.P[(long long)gr + (long long)j * a.ldp] = v;
+    if (!(cqr_done && gr <= j)) a.P[(long long)gr + (long long)j * a.ldp] = v;   // CQR: R written
     a.Y[(long long)gr + (long long)j * a.ldy] = gr > j ? v : (gr == j ? 1.0 : 0.0);
   }
   for (int e = tid; e < R * nb; e += PANEL_THREADS) {     // Y^T: contiguous along j
@@ -498,7 +621,7 @@ panel_qr_kernel_t(const PanelArgs a) {
     double v = gr > j ? sc[j] * Ps[r * PANEL_LD + j] : (gr == j ? 1.0 : 0.0);
     a.Yt[(long long)j + (long long)gr * a.ldyt] = v;
   }
-  if (cta == tcta)
+  if (cta == tcta && !cqr_done)
     for (int e = tid; e < nb * nb; e += PANEL_THREADS) {
       int j = e / nb, i = e % nb;
       a.T[e] = Ts[j * PANEL_NB + i];
@@ -514,7 +637,7 @@ panel_qr_kernel_t(const PanelArgs a) {
       a.Yt[(long long)j + (long long)r * a.ldyt] = 0.0;
     }
   }
-  if (timed) {
+  if (timed && !cqr_done) {
     const int o = cta == 0 ? 0 : 4;
     for (int q = 0; q < 4; ++q) atomicAdd(a.dbg + o + q, ph[q]);
 #ifdef SDC_PANEL_SUBPHASES
@@ -536,9 +659,11 @@ inline int panel_rpt(int rows_per) {
 
 inline size_t panel_smem_bytes(int rows_per) {
   const int rpt = panel_rpt(rows_per);
-  return sizeof(double) * ((size_t)rows_per * PANEL_LD + (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB +
-                           2 * PANEL_NB + PANEL_NB * PANEL_NB + 36 * PANEL_NB + 2 +
-                           (rpt ? 2 * PANEL_RG * rpt + PANEL_NB : 0));
+  // after the row block: the Householder loop's scratch, or (aliased) the CQR path's
+  const size_t hh = (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB + 2 * PANEL_NB + PANEL_NB * PANEL_NB +
+                    36 * PANEL_NB + 2;
+  const size_t scratch = rpt ? std::max(hh, (size_t)CQ_SCRATCH) : hh;
+  return sizeof(double) * ((size_t)rows_per * PANEL_LD + scratch + (rpt ? 2 * PANEL_RG * rpt + PANEL_NB : 0));
 }
 
 #undef PSTAMP

@@ -99,6 +99,9 @@ struct sdc_handle {
   size_t bat_out_n = 0;
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
   double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
+  double* cqbuf = nullptr;             // CholeskyQR2 panel exchange slots (CQ_DOUBLES)
+  bool cqr = true;                     // CholeskyQR2 panels (SDC_CQR=0: Householder only)
+  unsigned long long* cqstat = nullptr;   // device: [0] CQR panels done, [1] fallbacks
   unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
   double *pmA = nullptr, *pmB = nullptr, *vec = nullptr, *scal = nullptr;
   size_t wp_elems = 0;
@@ -131,7 +134,11 @@ struct sdc_handle {
   bool xpass_on = false;               // cross-pass look-ahead in the fixed-mode pass loop
                                        // (SDC_XPASS=1; measured no gain: the first panels'
                                        // cluster waits for the products' CTAs to drain)
-  int side_reserve = 0;                // SMs the side stream's persistent GEMMs leave free
+  // GEMM schedule knobs (env at sdc_create; DESIGN.md §6 table): persistent grids for short-K
+  // updates (0 off, 1 short-K, 2 every TMA GEMM), bulk reduce-add epilogue for beta = 1,
+  // persistent grids on the side stream / second chain too
+  int persist_mode = 1, red_mode = 1;
+  bool side_persist = false;
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
   double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
@@ -145,7 +152,7 @@ struct sdc_handle {
     double *Y = nullptr, *Yt = nullptr, *Tb = nullptr, *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr,
            *Gb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr, *llbuf = nullptr,
            *vec = nullptr, *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr, *C = nullptr, *G1 = nullptr,
-           *G2 = nullptr, *G3 = nullptr;
+           *G2 = nullptr, *G3 = nullptr, *cqbuf = nullptr;
     unsigned int* bar = nullptr;
     unsigned long long bar_count = 0;
     unsigned ll_epoch = 0;
@@ -223,6 +230,7 @@ void swap_ctx(sdc_handle* h) {
   std::swap(h->bar, a.bar); std::swap(h->bar_count, a.bar_count); std::swap(h->ll_epoch, a.ll_epoch);
   std::swap(h->C, a.C); std::swap(h->G1, a.G1); std::swap(h->G2, a.G2); std::swap(h->G3, a.G3);
   std::swap(h->gemm_force, a.gemm_force);
+  std::swap(h->cqbuf, a.cqbuf);
   std::swap(h->xpass_pending, a.xpass_pending);
 }
 struct AltScope {   // issue on the second context for the scope's lifetime
@@ -392,14 +400,6 @@ double tma_gemm_work(const TmaGemmArgs& g) {
   return 2.0 * M * cols;
 }
 
-int gemm_variant_override() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("SDC_GEMM_VARIANT");
-    v = e ? atoi(e) : -1;
-  }
-  return v;
-}
 
 template <class T>
 int launch_tma_t(sdc_handle* h, const double* A, long long lda, const double* B, long long ldb,
@@ -445,43 +445,13 @@ int launch_tma_persist(sdc_handle* h, const double* A, long long lda, const doub
     return SDC_ERR_CUDA;
   }
   const long long tiles = (long long)cdiv(g.M, T::BM) * cdiv(g.N, T::BN) * splits;
-  // on the look-ahead side stream the persistent CTAs leave side_reserve SMs to the
-  // critical chain (panels, next-block updates), whose kernels would otherwise queue behind
-  // CTAs that do not retire until the whole update is done
-  const int sms = h->on_side ? std::max(1, h->num_sms - h->side_reserve) : h->num_sms;
-  const int grid = (int)std::min<long long>(tiles, (long long)sms * T::MINB);
+  const int grid = (int)std::min<long long>(tiles, (long long)h->num_sms * T::MINB);
   ProfScope ps(h, SDC_PROF_GEMM, tma_gemm_work(g), h->gemm_sub);
   gemm_tn_tma_persist_kernel<T><<<grid, T::THREADS, smem, h->st>>>(tA, tB, g);
   SDC_LAUNCHED(h);
   return 0;
 }
 
-int red_mode() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("SDC_RED");
-    v = e ? atoi(e) : 1;   // bulk reduce-add epilogue for beta = 1 updates
-  }
-  return v;
-}
-
-int side_persist() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("SDC_SIDE_PERSIST");
-    v = e ? atoi(e) : 0;   // 0: one-tile CTAs for side-stream updates (default), 1: persistent
-  }
-  return v;
-}
-
-int persist_mode() {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("SDC_PERSIST");
-    v = e ? atoi(e) : 1;   // 0 off, 1 short-K updates, 2 every TMA GEMM
-  }
-  return v;
-}
 
 // C = alpha A_s^T B_s + beta C  [+ D2 = alpha2 A_s^T B_s];  K-split into `splits` slices of
 // kchunk (multiple of 16) written to C + z * c_zstride when splits > 1.
@@ -495,7 +465,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (tma) {
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
                   (int)(al16(C, ldc) && M % 2 == 0), kupper};
-    int v = h->gemm_force >= 0 ? h->gemm_force : gemm_variant_override();
+    int v = h->gemm_force;
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
       if (M <= 64) v = 1;
@@ -505,13 +475,13 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
       else v = 2;
     }
     if (v == 4 && !cok) v = 0;
-    const int pm = persist_mode();
+    const int pm = h->persist_mode;
     // On the look-ahead side stream the short-K updates use one-tile CTAs: a persistent grid
     // would hold every SM until the whole update finished, and the critical chain's kernels
     // (panels, next-block updates, reductions) on the high-priority stream would queue
     // behind it; one-tile CTAs retire continuously, so the scheduler can hand SMs to them.
-    if (v == 3 && (h->on_side || h->two_chains) && side_persist() == 0) {
-      if (red_mode() && beta == 1.0 && D2 == nullptr && g.red_ok)
+    if (v == 3 && (h->on_side || h->two_chains) && !h->side_persist) {
+      if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
         return launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
       return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
     }
@@ -521,7 +491,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
         case 1: return launch_tma_persist<TmaM>(h, A, lda, B, ldb, g, splits);
         case 2: return launch_tma_persist<TmaS>(h, A, lda, B, ldb, g, splits);
         case 3:
-          if (red_mode() && beta == 1.0 && D2 == nullptr && g.red_ok)
+          if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
             return launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
           return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
         default: break;
@@ -688,8 +658,12 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     }
     cur = smem;
   }
+  // CholeskyQR2 first (register variants in cluster mode, full-width panels), Householder on
+  // breakdown (cqr.cuh)
+  const int use_cqr = h->cqr && cluster && rpt > 0 && nb == NB && G <= CQ_GMAX ? 1 : 0;
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
-              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize, h->llbuf, h->ll_epoch};
+              rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize, h->llbuf, h->ll_epoch,
+              h->cqbuf, use_cqr, h->cqstat};
   ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * nb);   // read panel, write panel + Y + Y^T
   if (cluster) {
     cudaLaunchConfig_t cfg = {};
@@ -706,7 +680,8 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     cfg.numAttrs = 1;
     void* args[] = {&a};
     SDC_CK(cudaLaunchKernelExC(&cfg, fn, args));
-    if (G > csize) h->ll_epoch += nb;
+    if (G > csize || use_cqr) h->ll_epoch += nb;
+    if (use_cqr) h->sched[SDC_SCHED_PANEL_CQR_TRIED]++;
     h->sched[G > csize ? SDC_SCHED_PANEL_MCLUSTER : SDC_SCHED_PANEL_CLUSTER]++;
   } else {
     void* args[] = {&a};
@@ -1133,12 +1108,14 @@ int similarity_select(sdc_handle* h, int n, const double* A, long long lda, cons
 int reset_sync(sdc_handle* h) {
   SDC_CK(cudaMemsetAsync(h->bar, 0, 64, h->st));
   SDC_CK(cudaMemsetAsync(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
+  SDC_CK(cudaMemsetAsync(h->cqbuf, 0, CQ_DOUBLES * sizeof(double), h->st));
   h->bar_count = 0;
   h->ll_epoch = 0;
   h->xpass_pending = h->alt.xpass_pending = false;
   if (h->alt_ready) {   // (on the caller's stream: ordered before any fork to the context)
     SDC_CK(cudaMemsetAsync(h->alt.bar, 0, 64, h->st));
     SDC_CK(cudaMemsetAsync(h->alt.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double), h->st));
+    SDC_CK(cudaMemsetAsync(h->alt.cqbuf, 0, CQ_DOUBLES * sizeof(double), h->st));
     h->alt.bar_count = 0;
     h->alt.ll_epoch = 0;
   }
@@ -1166,6 +1143,7 @@ int ensure_alt(sdc_handle* h) {
   ALLOC(a.W, (size_t)std::max(256, h->nbo_max) * (n + 64));
   ALLOC(a.gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
   ALLOC(a.llbuf, PANEL_LL_DOUBLES);
+  ALLOC(a.cqbuf, CQ_DOUBLES);
   ALLOC(a.vec, 4 * n + 64);
   ALLOC(a.C, 2 * nn);
   ALLOC(a.G1, nn); ALLOC(a.G2, nn); ALLOC(a.G3, nn);
@@ -1194,6 +1172,7 @@ int ensure_alt(sdc_handle* h) {
   a.bar = (unsigned*)q;
   SDC_CK(cudaMemset(a.bar, 0, 64));
   SDC_CK(cudaMemset(a.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)));
+  SDC_CK(cudaMemset(a.cqbuf, 0, CQ_DOUBLES * sizeof(double)));
   SDC_CK(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
   if (h->lookahead) {
     int least = 0, greatest = 0;
@@ -1395,8 +1374,20 @@ int sdc_debug_counters(sdc_handle* h, unsigned long long* out, int count, int re
 int sdc_schedule_counters(sdc_handle* h, long long* out, int count, int reset) {
   if (!h) { set_err("null handle"); return -1; }
   if (count < 0 || count > SDC_SCHED_COUNTERS || (count > 0 && !out)) { set_err("bad count"); return -3; }
+  if (count > SDC_SCHED_PANEL_CQR_DONE) {   // device-side outcomes of the CholeskyQR2 panels
+    DevGuard dg_;
+    SDC_TRY(check_handle(h, &dg_));
+    unsigned long long st[2] = {0, 0};
+    SDC_CK(cudaDeviceSynchronize());
+    SDC_CK(cudaMemcpy(st, h->cqstat, sizeof(st), cudaMemcpyDeviceToHost));
+    h->sched[SDC_SCHED_PANEL_CQR_DONE] = (long long)st[0];
+    h->sched[SDC_SCHED_PANEL_CQR_FALLBACK] = (long long)st[1];
+  }
   for (int i = 0; i < count; ++i) out[i] = h->sched[i];
-  if (reset) for (int i = 0; i < SDC_SCHED_COUNTERS; ++i) h->sched[i] = 0;
+  if (reset) {
+    for (int i = 0; i < SDC_SCHED_COUNTERS; ++i) h->sched[i] = 0;
+    cudaMemset(h->cqstat, 0, 16);
+  }
   return 0;
 }
 
@@ -1502,6 +1493,8 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   ALLOC(h->gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
   ALLOC(h->llbuf, PANEL_LL_DOUBLES);
   if (!rc && cudaMemset(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)) != cudaSuccess) rc = SDC_ERR_CUDA;
+  ALLOC(h->cqbuf, CQ_DOUBLES);
+  if (!rc && cudaMemset(h->cqbuf, 0, CQ_DOUBLES * sizeof(double)) != cudaSuccess) rc = SDC_ERR_CUDA;
   ALLOC(h->pmA, (n / SEL_T + 1) * n);
   if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
   ALLOC(h->vec, 4 * n + 64);
@@ -1518,9 +1511,15 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     if (cudaMalloc(&q, 64 * sizeof(unsigned long long)) != cudaSuccess) rc = SDC_ERR_NOMEM;
     else { h->allocs.push_back(q); h->dbg = (unsigned long long*)q; cudaMemset(q, 0, 64 * 8); }
   }
+  if (!rc) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, 2 * sizeof(unsigned long long)) != cudaSuccess) rc = SDC_ERR_NOMEM;
+    else { h->allocs.push_back(q); h->cqstat = (unsigned long long*)q; cudaMemset(q, 0, 16); }
+  }
   if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
   if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
   if (getenv("SDC_PANEL_SMEM")) h->panel_reg = false;
+  if (const char* e = getenv("SDC_CQR")) h->cqr = atoi(e) != 0;
   if (const char* e = getenv("SDC_GRAPH_MAX_N")) h->graph_max_n = atoi(e);
   if (const char* e = getenv("SDC_CLUSTER_MAX_ROWS")) h->cluster_max_rows = atoi(e);
   if (!rc) {   // non-portable cluster size 16 for the small-panel kernel (if the part allows it)
@@ -1567,7 +1566,10 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaMallocHost(&h->hflags, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
   if (!rc && cudaStreamCreateWithFlags(&h->cap_st, cudaStreamNonBlocking) != cudaSuccess) rc = SDC_ERR_CUDA;
   if (const char* e = getenv("SDC_LOOKAHEAD")) h->lookahead = atoi(e) != 0;
-  if (const char* e = getenv("SDC_SIDE_RESERVE")) h->side_reserve = std::max(0, atoi(e));
+  if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
+  if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
+  if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
+  if (const char* e = getenv("SDC_GEMM_VARIANT")) h->gemm_force = h->alt.gemm_force = atoi(e);
   if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
   if (getenv("SDC_ALT_FAIL_ALLOC")) h->alt_fail_hook = true;
@@ -1657,7 +1659,8 @@ int schur_node(sdc_handle* h, cudaStream_t st, int m, double* Tb, long long ldtb
                              (int)ldqb, nullptr, 0, w.Ab, m, nullptr, 0, &res));
     h->st = st;
     stats[3] += res.iters;
-    const bool onesided = res.side < 1e-6 || res.side > 1.0 - 1e-6;
+    // accept only clearly two-sided pairs (same rule as orc_schur_node; reading Q20)
+    const bool onesided = res.side < 1e-3 || res.side > 1.0 - 1e-3;
     if (res.status != 0 || onesided) {   // a one-sided pair's split is incidental
       stats[1]++;
       if (res.side > 0.95) hi = a;          // every eigenvalue left of the line
@@ -1816,12 +1819,8 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
   if (batch == 0) return 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->st = st;
-  static const bool v1 = getenv("SDC_BATCHED_V1") != nullptr;   // unblocked variant (A/B)
-  const size_t smem = v1 ? bat_smem_doubles() * sizeof(double) : bq_smem_bytes(BAT_NMAX);
   static DevOnce attr;
   if (!attr.has(h->device)) {
-    SDC_CK(cudaFuncSetAttribute(k_split_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(bat_smem_doubles() * sizeof(double))));
     SDC_CK(cudaFuncSetAttribute(k_split_batched_wy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)bq_smem_bytes(BAT_NMAX)));
     attr.set(h->device);
@@ -1837,8 +1836,7 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
     h->bat_out_n = (size_t)batch * 4;
   }
   BatArgs a{A, lda, strideA, V, ldv, strideV, Q, ldq, strideQ, h->bat_out, n, max_iters};
-  if (v1) k_split_batched<<<batch, BAT_THREADS, smem, st>>>(a);
-  else k_split_batched_wy<<<batch, BQ_THREADS, bq_smem_bytes(n), st>>>(a);
+  k_split_batched_wy<<<batch, BQ_THREADS, bq_smem_bytes(n), st>>>(a);
   SDC_LAUNCHED(h);
   std::vector<double> out((size_t)batch * 4);
   SDC_CK(cudaMemcpyAsync(out.data(), h->bat_out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, st));

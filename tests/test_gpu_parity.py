@@ -423,3 +423,38 @@ def test_panel_exchange_modes_parity(orc, sdc, env):
     else:
         assert c["panel_cluster"] > 0 and c["panel_grid"] == 0, c
     assert_parity(o, Q, info, p.A, p.n, Ah)
+
+
+# ---------------------------------------------------------------------------------------
+# schedule / kernel-variant knobs (DESIGN.md §6 table): every non-default variant the
+# library can run gives the oracle's results
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("persist", [0, 1, 2])
+def test_forced_gemm_variants_vs_oracle(orc, sdc, variant, persist):
+    # SDC_GEMM_VARIANT forces one TMA tile shape for every GEMM (0 128x128, 1 64x128,
+    # 2 64x64, 3 128x64 two CTAs/SM, 4 128x128 with the C tile prefetched by TMA) and
+    # SDC_PERSIST picks one-tile vs persistent grids; beta = 1 exercises the reduce-add epilogue
+    h = _handle_with_env(sdc, 256, SDC_GEMM_VARIANT=variant, SDC_PERSIST=persist)
+    for (M, N, K, beta) in [(256, 192, 64, 1.0), (300, 257, 129, 0.5), (128, 640, 512, 0.0)]:
+        g = np.random.default_rng(M + N + K + variant)
+        a, b, c0 = g.standard_normal((K, M)), g.standard_normal((K, N)), g.standard_normal((M, N))
+        ref = orc.gemm(a, b, True, False) + beta * c0
+        c = dev(c0)
+        h.dgemm(dev(a), dev(b), True, False, alpha=1.0, beta=beta, C=c)
+        bound = (K + 2) * EPS * (orc.gemm(np.abs(a), np.abs(b), True, False) + abs(beta) * np.abs(c0))
+        assert np.all(np.abs(host(c) - ref) <= bound + 1e-300), (M, N, K)
+
+
+@pytest.mark.parametrize("env", [{"SDC_PERSIST": 0}, {"SDC_PERSIST": 2}, {"SDC_RED": 0},
+                                 {"SDC_SIDE_PERSIST": 1, "SDC_NBO": 128}, {"SDC_PANEL_SMEM": 1},
+                                 {"SDC_GEMM_VARIANT": 4}, {"SDC_CQR": 0}])
+def test_step_variants_parity(orc, sdc, env):
+    # the whole step with each non-default kernel variant (persistent grids off / everywhere,
+    # load-FMA-store instead of the bulk reduce-add epilogue, persistent side-stream updates,
+    # shared-memory panel loop instead of registers) on config 2's recipe at n = 600
+    h = _handle_with_env(sdc, 600, **env)
+    p = inputs.make_config(2, n=600)
+    Q, _, Ah, info, o = run_both(orc, h, p)
+    assert_parity(o, Q, info, p.A, p.n, Ah)
+    assert info.k == p.expected_k

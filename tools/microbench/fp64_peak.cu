@@ -1,6 +1,7 @@
 // Microbenchmark: FP64 tensor (DMMA m8n8k4) vs DFMA throughput on sm_100a.
 // Used once to pin the FP64 roofline figure.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int CHAINS>
@@ -65,12 +66,12 @@ __global__ void mixed_loop(double* out, int iters) {
   if (s == 12345.0) out[0] = s;
 }
 
-int main() {
+int main(int argc, char** argv) {
   double* d; cudaMalloc(&d, 8);
   int dev; cudaGetDevice(&dev); cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   printf("%s SMs=%d clock(kHz)=%d\n", p.name, p.multiProcessorCount, p.clockRate);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const int iters = 20000;
+  const int iters = argc > 1 ? atoi(argv[1]) : 20000;   // run_fp64_peak.sh: long enough to sample clocks
   for (int warps : {4, 8, 16}) {
     for (int bps : {1, 2}) {
       int blocks = p.multiProcessorCount * bps;
@@ -99,6 +100,8 @@ int main() {
     cudaEventRecord(e0);
     mixed_loop<<<blocks, warps * 32>>>(d, iters / 4);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
+    const cudaError_t e = cudaGetLastError();   // 16 warps x 64 DFMA chains: too many registers
+    if (e != cudaSuccess) { printf("MIXED warps=%2d: not launchable (%s)\n", warps, cudaGetErrorString(e)); continue; }
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     double flops = double(blocks) * warps * (iters / 4) * 4096.0;
     printf("MIXED warps=%2d: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
