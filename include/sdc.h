@@ -334,7 +334,9 @@ enum { SDC_SCHED_LOOKAHEAD_FORKS = 0,  /* look-ahead QR schedules forked to the 
        SDC_SCHED_PANEL_CQR_TRIED = 9,  /* panels launched with the CholeskyQR2 path first     */
        SDC_SCHED_PANEL_CQR_DONE = 10,  /* ... factored by it (device count; reading it syncs)  */
        SDC_SCHED_PANEL_CQR_FALLBACK = 11, /* ... that fell back to the Householder loop      */
-       SDC_SCHED_COUNTERS = 12 };
+       SDC_SCHED_GEMM_CPASYNC = 12,    /* step GEMMs staged by cp.async (an operand not 16-byte
+                                          aligned) instead of TMA                            */
+       SDC_SCHED_COUNTERS = 13 };
 /* Copies `count` (<= SDC_SCHED_COUNTERS) counters to the HOST array out; reset != 0 zeroes
  * them.  count > SDC_SCHED_PANEL_CQR_DONE synchronises the device (device-side counters).
  * Returns 0, -1 (null handle), -3 (bad count) or -100. */

@@ -168,17 +168,35 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
   double* mreg = a.cq + 2 * (size_t)CQ_REGION;
   const unsigned f1 = a.epoch + 1u, f2 = a.epoch + 2u, f3 = a.epoch + 3u;
   const int eper = (CQ_E + G - 1) / G, e0 = min(CQ_E, cta * eper), e1 = min(CQ_E, e0 + eper);
+  // phase timers (SDC_DEBUG_COUNTERS): CTA 0 -> dbg[32..47], last CTA -> dbg[48..63]
+  const bool tmd = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
+  unsigned long long tq = tmd ? clock64() : 0ull;
+  int ph = 0;
+  auto stamp = [&]() {
+    if (tmd) {
+      const unsigned long long t = clock64();
+      atomicAdd(a.dbg + (cta == 0 ? 32 : 48) + ph, t - tq);
+      tq = t;
+    }
+    ++ph;
+  };
   // (1) G1 = P^T P (owner-reduced through L2), R1 = chol(G1)
   cq_gram_partial(Ps, PANEL_LD, R, reg0 + 2 * (size_t)cta * CQ_E, f1);
+  stamp();                                             // 0: Gram 1 partial (thread 0's warp)
   cq_owner_reduce(reg0, G, e0, e1, f1, err);
+  stamp();                                             // 1: owner reduce
   cq_gather<true>(reg0 + 2 * (size_t)G * CQ_E, f1, Am, err);
   __syncthreads();
+  stamp();                                             // 2: gather
   if (!cq_chol(Am, gd, dv)) return 1;
+  stamp();                                             // 3: chol 1
   // (2) Q1 = P R1^{-1} in place; keep R1 (transposed into Bm's lower part, diagonal in r1d)
   cq_trinv_upper(Am, Bm);
   __syncthreads();
+  stamp();                                             // 4: R1^{-1}
   cq_rows_times_upper(Ps, PANEL_LD, R, 0, Bm);
   __syncthreads();
+  stamp();                                             // 5: Q1 = P R1^{-1}
   for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
     const int i = e & 63, j = e >> 6;
     if (i < j) Bm[j + i * CQ_LD] = Am[i + j * CQ_LD];
@@ -186,16 +204,21 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
   }
   __syncthreads();
   // (3) G2 = Q1^T Q1, R2 = chol(G2)
+  stamp();                                             // 6: keep R1
   cq_gram_partial(Ps, PANEL_LD, R, reg1 + 2 * (size_t)cta * CQ_E, f2);
   cq_owner_reduce(reg1, G, e0, e1, f2, err);
   cq_gather<true>(reg1 + 2 * (size_t)G * CQ_E, f2, Am, err);
   __syncthreads();
+  stamp();                                             // 7: Gram 2 (partial + exchange)
   if (!cq_chol(Am, gd, dv)) return 2;
+  stamp();                                             // 8: chol 2
   if (cta == 0) {
     // (4) Q_top = Q1(0:64,:) R2^{-1}; Q_top - D = L U; R = D R2 R1 -> P(0:64, 0:64) upper
     cq_trsm_rows64(Ps, PANEL_LD, Am);
     __syncthreads();
+    stamp();                                           // 9: Q_top
     cq_lu_signed(Ps, PANEL_LD, dsg, ukk);
+    stamp();                                           // 10: LU
     for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
       const int i = e & 63, j = e >> 6;
       if (i > j) continue;
@@ -219,6 +242,7 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
       const int j = cq_col(p), i = p - j * (j + 1) / 2;
       cq_ll_store(mreg + 2 * (size_t)p, Am[i + j * CQ_LD], f3);
     }
+    stamp();                                           // 11: R, W, M published
     // (6) T = -U D L^{-T} (upper), tau = diag T
     cq_trinv_unit_lower(Ps, PANEL_LD, Bm);
     __syncthreads();
@@ -231,12 +255,15 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
       if (i == j) a.tau[i] = -acc;
     }
   } else {
+    ph = 12;
     cq_gather<false>(mreg, f3, Am, err);
   }
   __syncthreads();
+  stamp();                                             // 12: T (CTA 0) / wait for M (others)
   // (7) Y(64:m, :) = Q1 M for the rows below the panel's top 64
   cq_rows_times_upper(Ps, PANEL_LD, R, cta == 0 ? 64 : 0, Am);
   __syncthreads();
+  stamp();                                             // 13: Y = Q1 M
   return 0;
 }
 

@@ -100,7 +100,7 @@ struct sdc_handle {
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
   double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
   double* cqbuf = nullptr;             // CholeskyQR2 panel exchange slots (CQ_DOUBLES)
-  bool cqr = true;                     // CholeskyQR2 panels (SDC_CQR=0: Householder only)
+  bool cqr = false;                    // CholeskyQR2 panels (SDC_CQR=1; off until faster)
   unsigned long long* cqstat = nullptr;   // device: [0] CQR panels done, [1] fallbacks
   unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
   double *pmA = nullptr, *pmB = nullptr, *vec = nullptr, *scal = nullptr;
@@ -240,6 +240,9 @@ struct AltScope {   // issue on the second context for the scope's lifetime
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+// leading dimension of the n x n workspace matrices: n rounded up to even, so that every
+// column starts 16-byte aligned and odd n keeps the TMA GEMM path
+inline long long wld(long long n) { return n + (n & 1); }
 inline bool al16(const void* p, long long ld) {
   return ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (ld % 2 == 0);
 }
@@ -506,6 +509,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
     }
   }
   GemmArgs g{M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride};
+  h->sched[SDC_SCHED_GEMM_CPASYNC]++;   // operands not 16-byte aligned: cp.async staging
   return launch_gemm_tile<true, false>(h, g, splits);
 }
 
@@ -927,8 +931,8 @@ int norms(sdc_handle* h, const double* X, long long ldx, int n, double* out2) {
   return 0;
 }
 
-Fac fac_stack(sdc_handle* h, int n) { return Fac{h->Y, 2LL * n, h->Yt, (long long)n}; }
-Fac fac_square(sdc_handle* h, int n) { return Fac{h->Y, (long long)n, h->Yt, (long long)n}; }
+Fac fac_stack(sdc_handle* h, int n) { return Fac{h->Y, 2LL * n, h->Yt, wld(n)}; }
+Fac fac_square(sdc_handle* h, int n) { return Fac{h->Y, wld(n), h->Yt, wld(n)}; }
 
 // ---------------------------------------------------------------------------------------
 // one IRS pass: S holds [B_j; -A_j]; writes A_{j+1}, B_{j+1} and the next stack into S
@@ -995,7 +999,7 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
 int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* Vt,
                 double* Q, long long ldq) {
   Nvtx nv("grurv_right (Alg. 1/2)");
-  const long long ld = n;
+  const long long ld = wld(n);
   const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
   SDC_LAUNCHED(h);                                                     // S = A_p + B_p
@@ -1017,7 +1021,7 @@ int grurv_right(sdc_handle* h, int n, const double* Ap, const double* Bp, const 
 int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const double* VLt,
                double* QL, long long ldq) {
   Nvtx nv("grurv_left (Alg. 4 l.4)");
-  const long long ld = n;
+  const long long ld = wld(n);
   const Fac f = fac_square(h, n);
   k_add<<<ew_grid((long long)n * n), 256, 0, h->st>>>(h->G1, ld, Ap, ld, Bp, ld, n, n);
   SDC_LAUNCHED(h);
@@ -1042,7 +1046,7 @@ int grurv_left(sdc_handle* h, int n, const double* Ap, const double* Bp, const d
 // leading column block X of Q_R, and QR preserves nested column spans.
 int ql_from_aq(sdc_handle* h, int n, const double* A, long long lda, const double* Q, long long ldq,
                double* QL, long long ldql) {
-  const long long ld = n;
+  const long long ld = wld(n);
   const Fac f = fac_square(h, n);
   SDC_TRY(transpose_rev(h, h->G3, ld, A, lda, n, 0));                   // A^T (K-major)
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->G3, ld, Q, ldq, 0.0, h->G2, ld));  // W = A Q_R
@@ -1077,7 +1081,7 @@ int similarity_select(sdc_handle* h, int n, const double* A, long long lda, cons
                       long long ldb, const double* Q, long long ldq, const double* QL,
                       long long ldql) {
   Nvtx nv("similarity + split selection");
-  const long long ld = n;
+  const long long ld = wld(n);
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, A, lda, QL, ldql, 0.0, h->T1, ld));     // G = A^T QL
   SDC_TRY(gemm_tn(h, n, n, n, 1.0, h->T1, ld, Q, ldq, 0.0, h->Ah, ld));    // G^T Q
   if (B) {
@@ -1126,7 +1130,7 @@ int reset_sync(sdc_handle* h) {
 int ensure_alt(sdc_handle* h) {
   if (h->alt_ready || !h->pipeline) return 0;
   auto& a = h->alt;
-  const size_t n = (size_t)h->n_max, nn = n * n;
+  const size_t n = (size_t)h->n_max, nn = (size_t)wld((long long)n) * n;   // n x n buffers with ld wld(n)
   int rc = 0;
   const size_t first_alloc = h->allocs.size();
 #define ALLOC(p, e) \
@@ -1236,7 +1240,7 @@ int check_handle(sdc_handle* h, DevGuard* g) {
 // ---------------------------------------------------------------------------------------
 int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const double* B, long long ldb,
                  const double* V, long long ldv, const double* VL, long long ldvl) {
-  const long long ld = n, m = 2LL * n;
+  const long long ld = wld(n), m = 2LL * n;
   const bool pencil = B != nullptr;
   SDC_TRY(reset_sync(h));
   h->b_ident = nullptr;
@@ -1282,7 +1286,7 @@ int enqueue_init(sdc_handle* h, int n, const double* A, long long lda, const dou
 int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const double* B, long long ldb,
                    double* Q, long long ldq, double* QLd, double* QL, long long ldql, double* Ahat,
                    long long ldah, bool have_split, int cur, int max_iters) {
-  const long long ld = n;
+  const long long ld = wld(n);
   const bool pencil = B != nullptr;
   if (!have_split) {
     const bool two = pencil && !h->ql_orth && h->alt_ready;   // left GRURV on the second context
@@ -1321,7 +1325,7 @@ int enqueue_fixed(sdc_handle* h, int n, const double* A, long long lda, const do
                   double* Q, long long ldq, double* QLd, double* QL, long long ldql, double* Ahat,
                   long long ldah, int max_iters) {
   // V/VL are read through the graph key's pointers; pass them via the handle's last key
-  const long long ld = n;
+  const long long ld = wld(n);
   const bool pencil = B != nullptr;
   SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, h->cur_V, h->cur_ldv, h->cur_VL, h->cur_ldvl));
   int cur = 0;
@@ -1459,7 +1463,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   h->n_max = n_max;
   h->pencil = pencil ? 1 : 0;
   h->num_sms = prop.multiProcessorCount;
-  const size_t n = (size_t)n_max, nn = n * n;
+  const size_t n = (size_t)n_max, nn = (size_t)wld((long long)n) * n;   // n x n buffers with ld wld(n)
   int rc = 0;
 #define ALLOC(p, e) \
   if (!rc) rc = dalloc(h, &(p), (e))
@@ -2024,7 +2028,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     // context while IRS pass j+1 runs on the caller's stream (issued before the host reads
     // pass j's metric; if pass j stops, that pass is discarded).  Same kernels on the same
     // inputs as the sequential order, so the results are bit-identical to it.
-    const long long ld = n;
+    const long long ld = wld(n);
     struct Share {   // GRURV(j) panels on the second context run next to pass j+1's panels
       sdc_handle* h;
       explicit Share(sdc_handle* h_) : h(h_) { h->share_sms = true; }
@@ -2072,7 +2076,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     SDC_TRY(enqueue_finish(h, n, A, lda, B, ldb, Q, ldq, QLd, QL, ldql, Ahat, ldah, have_split, cur, max_iters));
   } else {
     // RTEST / E21: host decisions between passes (one scalar D2H per pass)
-    const long long ld = n;
+    const long long ld = wld(n);
     SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
     int cur = 0;
     bool have_split = false;
@@ -2188,7 +2192,7 @@ int sdc_qr(sdc_handle* h, void* stream, int m, int n, double* A, int lda, double
   choose_nbo(h, n);
   h->st = static_cast<cudaStream_t>(stream);
   SDC_TRY(reset_sync(h));
-  const Fac f{h->Y, (long long)m, h->Yt, (long long)n};
+  const Fac f{h->Y, wld(m), h->Yt, wld(n)};
   SDC_TRY(blocked_qr(h, A, lda, m, n, f));
   if (Qthin) {
     k_set_identity<<<ew_grid((long long)m * n), 256, 0, h->st>>>(Qthin, ldq, m, n, 1.0);
