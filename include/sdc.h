@@ -336,7 +336,11 @@ enum { SDC_SCHED_LOOKAHEAD_FORKS = 0,  /* look-ahead QR schedules forked to the 
        SDC_SCHED_PANEL_CQR_FALLBACK = 11, /* ... that fell back to the Householder loop      */
        SDC_SCHED_GEMM_CPASYNC = 12,    /* step GEMMs staged by cp.async (an operand not 16-byte
                                           aligned) instead of TMA                            */
-       SDC_SCHED_COUNTERS = 13 };
+       SDC_SCHED_MAX_CLUSTERS16 = 13,  /* (constant) 16-CTA panel clusters resident at once    */
+       SDC_SCHED_PANEL_MCLUSTER8 = 14, /* multi-cluster panels built from 8-CTA clusters (tall
+                                          stacks: keeps <= 256 rows per CTA in registers)    */
+       SDC_SCHED_GEMM_TMA = 15,        /* step GEMMs staged by TMA                              */
+       SDC_SCHED_COUNTERS = 16 };
 /* Copies `count` (<= SDC_SCHED_COUNTERS) counters to the HOST array out; reset != 0 zeroes
  * them.  count > SDC_SCHED_PANEL_CQR_DONE synchronises the device (device-side counters).
  * Returns 0, -1 (null handle), -3 (bad count) or -100. */

@@ -15,7 +15,8 @@ PROF_GEMM, PROF_PANEL, PROF_WYRED, PROF_SELECT, PROF_GEMM_W0, PROF_GEMM_UPD, PRO
 SPLIT_ACCEPT = 1e-8
 SCHED_NAMES = ("lookahead_forks", "xpass_forks", "ctx_forks", "panel_cluster", "panel_mcluster",
                "panel_grid", "graph_captures", "graph_replays", "panel_mcluster_capped", "panel_cqr_tried",
-               "panel_cqr_done", "panel_cqr_fallback", "gemm_cpasync")
+               "panel_cqr_done", "panel_cqr_fallback", "gemm_cpasync", "max_clusters16",
+               "panel_mcluster8", "gemm_tma")
 
 
 class SdcResult(ctypes.Structure):

@@ -30,7 +30,7 @@ constexpr int CQ_E = 64 * 65 / 2;         // packed upper triangle of a 64 x 64 
 constexpr int CQ_GMAX = 160;              // most CTAs of one panel
 constexpr int CQ_REGION = (CQ_GMAX + 1) * CQ_E * 2;          // doubles: partials + reduced (LL)
 constexpr size_t CQ_DOUBLES = 2 * (size_t)CQ_REGION + 2 * CQ_E + 64;   // exchange buffer per context
-constexpr int CQ_SCRATCH = 2 * 64 * CQ_LD + 6 * 64;          // shared doubles used by the path
+constexpr int CQ_SCRATCH = 2 * 64 * CQ_LD + 2 * 64 + 512 + 8;  // shared doubles used by the path
 constexpr double CQ_PIVOT_TOL = 1e-6;
 
 SDC_DEV int cq_col(int p) {               // column j of packed upper index p = j(j+1)/2 + i
@@ -88,8 +88,8 @@ SDC_DEV void cq_gram_partial(const double* X, int ldx, int R, double* slot, unsi
   double acc[2][2][2] = {};
   const int K = (R + 3) & ~3;
   cq_tile16(acc, 0, K,
-            [&](int i, int k) { return k < R ? X[k * ldx + 16 * bi + i] : 0.0; },
-            [&](int k, int j) { return k < R ? X[k * ldx + 16 * bj + j] : 0.0; });
+            [=](int i, int k) { return k < R ? X[k * ldx + 16 * bi + i] : 0.0; },
+            [=](int k, int j) { return k < R ? X[k * ldx + 16 * bj + j] : 0.0; });
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
@@ -178,63 +178,6 @@ SDC_DEV void cq_gather(const double* red, unsigned flag, double* M, unsigned* er
   }
 }
 
-// ---- Cholesky (upper, G = R^T R) in place, right-looking with the unscaled pivot row:
-// one CTA barrier per step.  Returns false (every thread, same decision) if a pivot falls
-// below CQ_PIVOT_TOL of its column's squared norm gd[k] (kept in gd[]).
-SDC_DEV bool cq_chol(double* M, double* gd, double* dv) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int k = tid; k < 64; k += nt) gd[k] = M[k + k * CQ_LD];
-  __syncthreads();
-  for (int k = 0; k < 64; ++k) {
-    const double akk = M[k + k * CQ_LD];
-    if (!(akk > CQ_PIVOT_TOL * gd[k])) { __syncthreads(); return false; }
-    const double rinv = 1.0 / akk;
-    // trailing upper triangle (k < i <= j < 64): thread tid owns column j = tid & 63 and
-    // rows i = k + 1 + (tid >> 6) + 8 s
-    const int j = tid & 63;
-    if (j > k) {
-      const double akj = M[k + j * CQ_LD] * rinv;
-      for (int i = k + 1 + (tid >> 6); i <= j; i += 8) M[i + j * CQ_LD] -= M[k + i * CQ_LD] * akj;
-    }
-    __syncthreads();
-  }
-  // scale rows: R(k, j) = A(k, j) / sqrt(A_kk), j >= k; zero the strictly lower part
-  for (int k = tid; k < 64; k += nt) dv[k] = 1.0 / sqrt(M[k + k * CQ_LD]);
-  __syncthreads();
-  for (int e = tid; e < 64 * 64; e += nt) {
-    const int i = e & 63, j = e >> 6;
-    M[i + j * CQ_LD] = i <= j ? M[i + j * CQ_LD] * dv[i] : 0.0;
-  }
-  __syncthreads();
-  return true;
-}
-
-// ---- inverse of an upper triangular U (ld CQ_LD) into X (upper, ld CQ_LD), X != U:
-// columns are independent back substitutions; 8 threads per column (fixed-order shuffle sums)
-SDC_DEV void cq_trinv_upper(const double* U, double* X) {
-  const int j = threadIdx.x >> 3, q = threadIdx.x & 7;   // 64 columns x 8 threads
-  double x[8];                                            // x[s] = X(q + 8 s, j)
-#pragma unroll
-  for (int s = 0; s < 8; ++s) x[s] = 0.0;
-  for (int i = 63; i >= 0; --i) {                         // every lane runs every step (shuffles)
-    double part = 0.0;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int l = q + 8 * s;
-      if (l > i && l <= j) part = fma(U[i + l * CQ_LD], x[s], part);
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    part += __shfl_xor_sync(0xffffffffu, part, 4);
-    const double v = ((i == j ? 1.0 : 0.0) - part) / U[i + i * CQ_LD];
-#pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (q + 8 * s == i && i <= j) x[s] = v;
-  }
-#pragma unroll
-  for (int s = 0; s < 8; ++s) X[q + 8 * s + j * CQ_LD] = q + 8 * s <= j ? x[s] : 0.0;
-}
-
 // ---- rows of X (R rows, ld ldx, 64 columns) <- X * B, B upper triangular (ld CQ_LD), in
 // place: each warp owns 8-row stripes and reads its whole stripe before writing it
 SDC_DEV void cq_rows_times_upper(double* X, int ldx, int R, int rbeg, const double* B) {
@@ -255,91 +198,330 @@ SDC_DEV void cq_rows_times_upper(double* X, int ldx, int R, int rbeg, const doub
       }
     }
     __syncwarp();
-    const int orow = s0 + lr;
-    if (orow < R) {
+    if (row < R) {
 #pragma unroll
       for (int nj = 0; nj < 8; ++nj) {
-        X[orow * ldx + 8 * nj + 2 * lc] = acc[nj][0];
-        X[orow * ldx + 8 * nj + 2 * lc + 1] = acc[nj][1];
+        X[row * ldx + 8 * nj + 2 * lc] = acc[nj][0];
+        X[row * ldx + 8 * nj + 2 * lc + 1] = acc[nj][1];
       }
     }
   }
 }
 
-// ---- rows 0..63 of X (ld ldx) <- X(0:64, :) U^{-1}, U upper (ld CQ_LD): independent forward
-// substitutions per row, 8 threads per row (x_j = (x_j - sum_{l<j} x_l U_lj) / U_jj)
-SDC_DEV void cq_trsm_rows64(double* X, int ldx, const double* U) {
-  const int row = threadIdx.x >> 3, q = threadIdx.x & 7;
-  double x[8];
+// =======================================================================================
+// 64 x 64 building blocks (CTA of 512 threads = 16 warps; matrices col-major in shared
+// memory, X(i, j) = X[i + j * ld]).  The serial parts (a 64-step pivot chain) are factored
+// in 16 x 16 diagonal blocks by ONE warp in registers (lane j holds column j; shuffles, no
+// barriers), everything off the diagonal blocks is 16 x 16 DMMA tiles -- a few CTA barriers
+// per 64 x 64 factorisation instead of one per pivot.
+// =======================================================================================
+#define CQX(X, ld, i, j) (X)[(i) + (j) * (ld)]
+constexpr unsigned CQ_FULL = 0xffffffffu;
+
+// lane-column registers of the 16 x 16 block at (r0, c0): a[i] = X(r0 + i, c0 + (lane & 15))
+SDC_DEV void cq_blk_load(const double* X, int ld, int r0, int c0, double (&a)[16]) {
+  const int j = threadIdx.x & 15;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) x[s] = 0.0;
-  for (int j = 0; j < 64; ++j) {
-    double part = 0.0;
+  for (int i = 0; i < 16; ++i) a[i] = CQX(X, ld, r0 + i, c0 + j);
+}
+// store rows selected by `part` (0 all, 1 upper incl. diagonal, 2 strictly lower) of the
+// block; other rows of the block are written as zero when zero_rest
+SDC_DEV void cq_blk_store(double* X, int ld, int r0, int c0, const double (&a)[16], int part, bool zero_rest) {
+  const int lane = threadIdx.x & 31, j = lane & 15;
+  if (lane >= 16) return;
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (q + 8 * s < j) part = fma(x[s], U[(q + 8 * s) + j * CQ_LD], part);
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    part += __shfl_xor_sync(0xffffffffu, part, 4);
-    const double v = (X[row * ldx + j] - part) / U[j + j * CQ_LD];
-#pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (q + 8 * s == j) x[s] = v;
+  for (int i = 0; i < 16; ++i) {
+    const bool keep = part == 0 || (part == 1 ? i <= j : i > j);
+    if (keep) CQX(X, ld, r0 + i, c0 + j) = a[i];
+    else if (zero_rest) CQX(X, ld, r0 + i, c0 + j) = 0.0;
   }
-  __syncwarp();
-#pragma unroll
-  for (int s = 0; s < 8; ++s) X[row * ldx + q + 8 * s] = x[s];
 }
 
-// ---- modified LU without pivoting (dorhr_col): X(0:64, 0:64) (ld ldx) - D = L U in place,
-// D_k = -sign(pivot) so that |U_kk| = |pivot| + 1 >= 1; one CTA barrier per step.  On return
-// X holds L (strictly lower, unit diagonal implied) and U (upper); D in dsg, U_kk in ukk.
-SDC_DEV void cq_lu_signed(double* X, int ldx, double* dsg, double* ukk) {
-  const int tid = threadIdx.x;
-  const int j = tid & 63, i0 = tid >> 6;
-  for (int k = 0; k < 64; ++k) {
-    const double piv = X[k * ldx + k];
+// one warp: upper Cholesky of the 16 x 16 block in registers (a: lane j = column j); pivot k
+// must exceed CQ_PIVOT_TOL * gk[k] (its column's squared norm in the original Gram)
+SDC_DEV bool cq_chol16(double (&a)[16], const double* gk) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double piv = __shfl_sync(CQ_FULL, a[k], k);
+    ok = ok && piv > CQ_PIVOT_TOL * gk[k];
+    const double rd = piv > 0.0 ? rsqrt(piv) : 0.0;
+    a[k] *= rd;                                   // row k of R (columns >= k)
+#pragma unroll
+    for (int i = k + 1; i < 16; ++i) a[i] = fma(-__shfl_sync(CQ_FULL, a[k], i), a[k], a[i]);
+  }
+  return ok;
+}
+
+// one warp: x = U^{-1} for a 16 x 16 upper triangular block of the accessor u(i, j) (block
+// coordinates); unit != 0 assumes a unit diagonal.  Lane j returns column j of the inverse.
+template <class FU>
+SDC_DEV void cq_trinv16(FU u, bool unit, double (&x)[16]) {
+  const int j = threadIdx.x & 15;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = i == j ? 1.0 : 0.0;   // right-hand side e_j, solved in place
+#pragma unroll
+  for (int l = 15; l >= 0; --l) {
+    x[l] = unit ? x[l] : x[l] * __drcp_rn(u(l, l));
+#pragma unroll
+    for (int i = 0; i < l; ++i) x[i] = fma(-u(i, l), x[l], x[i]);
+  }
+}
+
+// one warp: modified LU (dorhr_col) of the 16 x 16 block in registers: pivot p -> p - s_k,
+// s_k = -sign(p); returns L (strictly lower, rows > k of column k), U (upper) in a; signs to
+// dsg[0..16) (lane 0)
+SDC_DEV void cq_lu16(double (&a)[16], double* dsg) {
+  const int lane = threadIdx.x & 31, j = lane & 15;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const double piv = __shfl_sync(CQ_FULL, a[k], k);
     const double sk = piv >= 0.0 ? -1.0 : 1.0;
     const double pk = piv - sk;
-    if (tid == 0) { dsg[k] = sk; ukk[k] = pk; }
-    if (j > k) {
-      const double akj = X[k * ldx + j] / pk;
-      for (int i = k + 1 + i0; i < 64; i += 8) X[i * ldx + j] -= X[i * ldx + k] * akj;
+    const double rp = 1.0 / pk;                   // every lane (uniform, no divergent slow path)
+    if (lane == 0) dsg[k] = sk;
+#pragma unroll
+    for (int i = k + 1; i < 16; ++i) {           // l_ik from lane k's unscaled column
+      const double lik = __shfl_sync(CQ_FULL, a[i], k) * rp;
+      a[i] = j > k ? fma(-lik, a[k], a[i]) : (j == k ? a[i] * rp : a[i]);
     }
-    __syncthreads();
+    a[k] = j == k ? pk : a[k];
   }
-  for (int e = tid; e < 64 * 64; e += blockDim.x) {   // L = column k / U_kk, U_kk on the diagonal
-    const int r = e >> 6, c = e & 63;
-    if (r > c) X[r * ldx + c] /= ukk[c];
-    else if (r == c) X[r * ldx + c] = ukk[c];
-  }
+}
+
+// one warp: 16 x 16 tile product acc = op(A) op(B) over k in [0, K) (accessors in tile-local
+// row / column coordinates); D fragments per the PTX m8n8k4 layout
+template <class FA, class FB>
+SDC_DEV void cq_mm16(double (&acc)[2][2][2], int K, FA fa, FB fb) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) { acc[mi][ni][0] = 0.0; acc[mi][ni][1] = 0.0; }
+  cq_tile16(acc, 0, K, fa, fb);
+}
+template <class FS>
+SDC_DEV void cq_acc_store(const double (&acc)[2][2][2], FS st) {
+  const int lane = threadIdx.x & 31, lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) st(8 * mi + lr, 8 * ni + 2 * lc + c, acc[mi][ni][c]);
+}
+
+// ---- C(64 x 64) = alpha A B with accessors; every warp one 16 x 16 tile, the K loop of tile
+// (ti, tj) restricted to [16 kl(ti, tj), 16 kh(ti, tj)) (triangular operands); the products
+// are formed in registers and stored after a CTA barrier, so C may alias A or B
+template <class FA, class FB, class FKL, class FKH, class FS>
+SDC_DEV void cq_gemm64(FA fa, FB fb, FKL kl, FKH kh, double alpha, FS st) {
+  const int w = threadIdx.x >> 5, ti = w >> 2, tj = w & 3;
+  double acc[2][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) { acc[mi][ni][0] = 0.0; acc[mi][ni][1] = 0.0; }
+  cq_tile16(acc, 16 * kl(ti, tj), 16 * kh(ti, tj), [=](int i, int k) { return fa(16 * ti + i, k); },
+            [=](int k, int j) { return fb(k, 16 * tj + j); });
+  __syncthreads();
+  cq_acc_store(acc, [=](int i, int j, double v) { st(16 * ti + i, 16 * tj + j, alpha * v); });
   __syncthreads();
 }
 
-// ---- inverse of the unit lower triangular L (strictly lower part of X rows 0..63, ld ldx)
-// into Li (lower, unit diagonal, zero upper; ld CQ_LD): 8 threads per column
-SDC_DEV void cq_trinv_unit_lower(const double* X, int ldx, double* Li) {
-  const int j = threadIdx.x >> 3, q = threadIdx.x & 7;
-  double x[8];
+// ---- one warp, lanes 0..15 own the columns of the 16 x 16 tile B (block coordinates via
+// the accessor): B <- U^{-T} B for U upper (forward substitution, rinv = 1/diag), or
+// B <- L^{-1} B for L unit lower (accessor l(i, k), i > k).  16-step chains of FMAs with
+// broadcast shared-memory operands, no shuffles.
+template <class FU, class FB>
+SDC_DEV void cq_solve_cols_ut(FU u, const double* rinv, FB b) {
+  const int j = threadIdx.x & 31;
+  if (j >= 16) return;
+  double x[16];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) x[s] = 0.0;
-  for (int i = 0; i < 64; ++i) {
-    double part = 0.0;
+  for (int i = 0; i < 16; ++i) x[i] = b(i, j);
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int l = q + 8 * s;
-      if (l >= j && l < i) part = fma(X[i * ldx + l], x[s], part);
-    }
-    part += __shfl_xor_sync(0xffffffffu, part, 1);
-    part += __shfl_xor_sync(0xffffffffu, part, 2);
-    part += __shfl_xor_sync(0xffffffffu, part, 4);
-    const double v = i == j ? 1.0 : -part;
+  for (int i = 0; i < 16; ++i) {                 // (U^T x)_i = sum_{k <= i} U(k, i) x_k
 #pragma unroll
-    for (int s = 0; s < 8; ++s)
-      if (q + 8 * s == i && i >= j) x[s] = v;
+    for (int k = 0; k < i; ++k) x[i] = fma(-u(k, i), x[k], x[i]);
+    x[i] *= rinv[i];
   }
 #pragma unroll
-  for (int s = 0; s < 8; ++s) Li[q + 8 * s + j * CQ_LD] = q + 8 * s >= j ? x[s] : 0.0;
+  for (int i = 0; i < 16; ++i) b(i, j) = x[i];
+}
+template <class FL, class FB>
+SDC_DEV void cq_solve_cols_unit_lower(FL l, FB b) {
+  const int j = threadIdx.x & 31;
+  if (j >= 16) return;
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = b(i, j);
+#pragma unroll
+  for (int i = 1; i < 16; ++i)
+#pragma unroll
+    for (int k = 0; k < i; ++k) x[i] = fma(-l(i, k), x[k], x[i]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) b(i, j) = x[i];
+}
+// rows of B (16 x 16, lanes own rows) <- B U^{-1}, U upper: x_j = (b_j - sum_{k<j} x_k U(k,j)) / U(j,j)
+template <class FU, class FB>
+SDC_DEV void cq_solve_rows_upper(FU u, const double* rinv, FB b) {
+  const int i = threadIdx.x & 31;
+  if (i >= 16) return;
+  double x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) x[j] = b(i, j);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+#pragma unroll
+    for (int k = 0; k < j; ++k) x[j] = fma(-x[k], u(k, j), x[j]);
+    x[j] *= rinv[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) b(i, j) = x[j];
+}
+
+// ---- upper Cholesky G = R^T R of the 64 x 64 A (ld CQ_LD) in place (strictly lower part
+// zeroed); false (every thread) on a pivot below CQ_PIVOT_TOL of its column's squared norm.
+// Per 16-block step K: warp 0 factors the diagonal block in registers, warps solve the row
+// panel R(K, J) = R_KK^{-T} A(K, J) tile by tile, DMMA tiles update the trailing blocks.
+// sc: >= 16 doubles of scratch; gd: 64 doubles (the original diagonal).
+__device__ __noinline__ bool cq_chol64(double* A, double* gd, double* sc, int* flag) {
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (tid < 64) gd[tid] = CQX(A, CQ_LD, tid, tid);
+  if (tid == 0) *flag = 1;
+  __syncthreads();
+  for (int K = 0; K < 4; ++K) {
+    const int o = 16 * K;
+    if (w == 0) {
+      double a[16];
+      cq_blk_load(A, CQ_LD, o, o, a);
+      if (!cq_chol16(a, gd + o) && tid == 0) *flag = 0;
+      cq_blk_store(A, CQ_LD, o, o, a, 1, true);
+      if (tid < 16) sc[tid] = 1.0 / a[tid];       // lane j's a[j] = R_jj
+    }
+    __syncthreads();
+    if (!*flag) return false;
+    if (K == 3) break;
+    if (w < 3 - K) {   // row panel tile J = K + 1 + w
+      const int c = o + 16 * (w + 1);
+      cq_solve_cols_ut([=](int i, int k) { return CQX(A, CQ_LD, o + i, o + k); }, sc,
+                       [=](int i, int j) -> double& { return CQX(A, CQ_LD, o + i, c + j); });
+    }
+    __syncthreads();
+    {   // trailing A(I, J) -= R(K, I)^T R(K, J), K < I <= J
+      int t = w, I = -1, J = -1;
+      for (int ii = K + 1; ii < 4 && I < 0; ++ii)
+        for (int jj = ii; jj < 4; ++jj) {
+          if (t == 0) { I = ii; J = jj; break; }
+          --t;
+        }
+      if (I >= 0) {
+        double acc[2][2][2];
+        cq_mm16(acc, 16, [=](int i, int k) { return CQX(A, CQ_LD, o + k, 16 * I + i); },
+                [=](int k, int j) { return CQX(A, CQ_LD, o + k, 16 * J + j); });
+        __syncwarp();
+        cq_acc_store(acc, [=](int i, int j, double v) { CQX(A, CQ_LD, 16 * I + i, 16 * J + j) -= v; });
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < 64 * 64; e += blockDim.x) {   // zero the strictly lower part
+    const int i = e & 63, j = e >> 6;
+    if (i > j) CQX(A, CQ_LD, i, j) = 0.0;
+  }
+  __syncthreads();
+  return true;
+}
+
+// ---- modified LU (dorhr_col) of the 64 x 64 A (ld lda) in place: A - D = L U, L unit lower
+// (strictly lower part), U upper; D to dsg.  sc: >= 16 doubles of scratch.
+__device__ __noinline__ void cq_lu64(double* A, int lda, double* dsg, double* sc) {
+  const int tid = threadIdx.x, w = tid >> 5;
+  for (int K = 0; K < 4; ++K) {
+    const int o = 16 * K;
+    if (w == 0) {
+      double a[16];
+      cq_blk_load(A, lda, o, o, a);
+      cq_lu16(a, dsg + o);
+      cq_blk_store(A, lda, o, o, a, 0, false);
+      if (tid < 16) sc[tid] = 1.0 / a[tid];       // lane j's a[j] = U_jj
+    }
+    __syncthreads();
+    if (K == 3) break;
+    if (w < 6 - 2 * K) {   // L(I, K) = A(I, K) U_KK^{-1} (rows), U(K, J) = L_KK^{-1} A(K, J) (columns)
+      const bool lpan = w < 3 - K;
+      const int b = 16 * (K + 1 + (lpan ? w : w - (3 - K)));
+      if (lpan)
+        cq_solve_rows_upper([=](int k, int j) { return CQX(A, lda, o + k, o + j); }, sc,
+                            [=](int i, int j) -> double& { return CQX(A, lda, b + i, o + j); });
+      else
+        cq_solve_cols_unit_lower([=](int i, int k) { return CQX(A, lda, o + i, o + k); },
+                                 [=](int i, int j) -> double& { return CQX(A, lda, o + i, b + j); });
+    }
+    __syncthreads();
+    {   // trailing A(I, J) -= L(I, K) U(K, J), I, J > K
+      const int nt = 3 - K;
+      if (w < nt * nt) {
+        const int I = 16 * (K + 1 + w / nt), J = 16 * (K + 1 + w % nt);
+        double acc[2][2][2];
+        cq_mm16(acc, 16, [=](int i, int k) { return CQX(A, lda, I + i, o + k); },
+                [=](int k, int j) { return CQX(A, lda, o + k, J + j); });
+        __syncwarp();
+        cq_acc_store(acc, [=](int i, int j, double v) { CQX(A, lda, I + i, J + j) -= v; });
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- X = U^{-1} for the 64 x 64 upper triangular accessor u (unit: unit diagonal), X col-major
+// (ld ldx, X must not alias u's storage): diagonal blocks by 4 warps, then two levels of
+// block merges X12 = -X11 U12 X22 with DMMA tiles
+template <class FU>
+__device__ __noinline__ void cq_trinv64(FU u, bool unit, double* X, int ldx) {
+  const int tid = threadIdx.x, w = tid >> 5;
+  if (w < 4) {
+    double x[16];
+    const int o = 16 * w;
+    cq_trinv16([=](int i, int j) { return u(o + i, o + j); }, unit, x);
+    cq_blk_store(X, ldx, o, o, x, 1, true);
+  }
+  for (int e = tid; e < 64 * 64; e += blockDim.x) {   // zero every block below the diagonal blocks
+    const int i = e & 63, j = e >> 6;
+    if ((i >> 4) > (j >> 4)) CQX(X, ldx, i, j) = 0.0;
+  }
+  __syncthreads();
+  // level 1: blocks (2b, 2b+1), b = 0, 1 (warps 0, 1)
+  if (w < 2) {
+    const int r = 32 * w, c = r + 16;
+    double acc[2][2][2];
+    cq_mm16(acc, 16, [=](int i, int k) { return u(r + i, c + k); },
+            [=](int k, int j) { return CQX(X, ldx, c + k, c + j); });        // U12 X22
+    __syncwarp();
+    cq_acc_store(acc, [=](int i, int j, double v) { CQX(X, ldx, r + i, c + j) = v; });
+    __syncwarp();
+    cq_mm16(acc, 16, [=](int i, int k) { return CQX(X, ldx, r + i, r + k); },
+            [=](int k, int j) { return CQX(X, ldx, r + k, c + j); });        // X11 (U12 X22)
+    __syncwarp();
+    cq_acc_store(acc, [=](int i, int j, double v) { CQX(X, ldx, r + i, c + j) = -v; });
+  }
+  __syncthreads();
+  // level 2: X(0:32, 32:64) = -X(0:32, 0:32) U(0:32, 32:64) X(32:64, 32:64)
+  double acc[2][2][2];
+  const int I = 16 * (w >> 1), J = 32 + 16 * (w & 1);
+  if (w < 4) {   // T = U(0:32, 32:64) X(32:64, 32:64) (X upper: K range 32 .. J + 16)
+    cq_mm16(acc, J + 16 - 32, [=](int i, int k) { return u(I + i, 32 + k); },
+            [=](int k, int j) { return CQX(X, ldx, 32 + k, J + j); });
+    __syncwarp();
+    cq_acc_store(acc, [=](int i, int j, double v) { CQX(X, ldx, I + i, J + j) = v; });
+  }
+  __syncthreads();
+  if (w < 4)     // X(I, J) = -X(I, 0:32) T(0:32, J) (X upper: K range I .. 32)
+    cq_mm16(acc, 32 - I, [=](int i, int k) { return CQX(X, ldx, I + i, I + k); },
+            [=](int k, int j) { return CQX(X, ldx, I + k, J + j); });
+  __syncthreads();
+  if (w < 4) cq_acc_store(acc, [=](int i, int j, double v) { CQX(X, ldx, I + i, J + j) = -v; });
+  __syncthreads();
 }
 
 }  // namespace sdc

@@ -158,10 +158,11 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
   double* Am = scr;                        // 64 x CQ_LD
   double* Bm = Am + 64 * CQ_LD;            // 64 x CQ_LD
   double* gd = Bm + 64 * CQ_LD;            // Cholesky column norms^2
-  double* dv = gd + 64;                    // 1 / sqrt(pivot)
-  double* r1d = dv + 64;                   // diag R1
-  double* dsg = r1d + 64;                  // D
-  double* ukk = dsg + 64;                  // U_kk
+  double* dsg = gd + 64;                   // D
+  double* sc = dsg + 64;                   // 512: diagonal-block inverses
+  int* flag = reinterpret_cast<int*>(sc + 512);
+  double* Cm = Ps;                         // CTA 0, after Q_top: rows 0..63 as a 64 x 64 (ld 65)
+  double* GS = a.T;                        // CTA 0: R1, then R2 R1 (global scratch; T at the end)
   unsigned* err = a.bar + 1;
   double* reg0 = a.cq;
   double* reg1 = a.cq + CQ_REGION;
@@ -180,6 +181,9 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
     }
     ++ph;
   };
+  auto up = [](int ti, int tj) { return ti; };            // K range of upper x upper tiles:
+  auto upk = [](int ti, int tj) { return tj + 1; };       //   blocks ti .. tj
+  auto k0 = [](int ti, int tj) { return 0; };
   // (1) G1 = P^T P (owner-reduced through L2), R1 = chol(G1)
   cq_gram_partial(Ps, PANEL_LD, R, reg0 + 2 * (size_t)cta * CQ_E, f1);
   stamp();                                             // 0: Gram 1 partial (thread 0's warp)
@@ -188,71 +192,59 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
   cq_gather<true>(reg0 + 2 * (size_t)G * CQ_E, f1, Am, err);
   __syncthreads();
   stamp();                                             // 2: gather
-  if (!cq_chol(Am, gd, dv)) return 1;
+  if (!cq_chol64(Am, gd, sc, flag)) return 1;
   stamp();                                             // 3: chol 1
-  // (2) Q1 = P R1^{-1} in place; keep R1 (transposed into Bm's lower part, diagonal in r1d)
-  cq_trinv_upper(Am, Bm);
-  __syncthreads();
+  // (2) Q1 = P R1^{-1} in place; CTA 0 keeps R1 in GS
+  cq_trinv64([=](int i, int j) { return CQX(Am, CQ_LD, i, j); }, false, Bm, CQ_LD);
   stamp();                                             // 4: R1^{-1}
   cq_rows_times_upper(Ps, PANEL_LD, R, 0, Bm);
+  if (cta == 0)
+    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) GS[e] = CQX(Am, CQ_LD, e & 63, e >> 6);
   __syncthreads();
   stamp();                                             // 5: Q1 = P R1^{-1}
-  for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
-    const int i = e & 63, j = e >> 6;
-    if (i < j) Bm[j + i * CQ_LD] = Am[i + j * CQ_LD];
-    else if (i == j) r1d[i] = Am[i + i * CQ_LD];
-  }
-  __syncthreads();
+  stamp();                                             // 6: (unused)
   // (3) G2 = Q1^T Q1, R2 = chol(G2)
-  stamp();                                             // 6: keep R1
   cq_gram_partial(Ps, PANEL_LD, R, reg1 + 2 * (size_t)cta * CQ_E, f2);
   cq_owner_reduce(reg1, G, e0, e1, f2, err);
   cq_gather<true>(reg1 + 2 * (size_t)G * CQ_E, f2, Am, err);
   __syncthreads();
   stamp();                                             // 7: Gram 2 (partial + exchange)
-  if (!cq_chol(Am, gd, dv)) return 2;
+  if (!cq_chol64(Am, gd, sc, flag)) return 2;
   stamp();                                             // 8: chol 2
   if (cta == 0) {
-    // (4) Q_top = Q1(0:64,:) R2^{-1}; Q_top - D = L U; R = D R2 R1 -> P(0:64, 0:64) upper
-    cq_trsm_rows64(Ps, PANEL_LD, Am);
-    __syncthreads();
-    stamp();                                           // 9: Q_top
-    cq_lu_signed(Ps, PANEL_LD, dsg, ukk);
+    // (4) R2^{-1}; R = R2 R1 (GS); Q_top = Q1(0:64,:) R2^{-1}; Q_top - D = L U
+    cq_trinv64([=](int i, int j) { return CQX(Am, CQ_LD, i, j); }, false, Bm, CQ_LD);
+    cq_gemm64([=](int i, int k) { return CQX(Am, CQ_LD, i, k); }, [=](int k, int j) { return GS[k + 64 * j]; },
+              up, upk, 1.0, [=](int i, int j, double v) { GS[i + 64 * j] = v; });
+    cq_gemm64([=](int i, int k) { return Ps[i * PANEL_LD + k]; }, [=](int k, int j) { return CQX(Bm, CQ_LD, k, j); },
+              k0, upk, 1.0, [=](int i, int j, double v) { CQX(Am, CQ_LD, i, j) = v; });
+    stamp();                                           // 9: R2^{-1}, R, Q_top
+    cq_lu64(Am, CQ_LD, dsg, sc);
     stamp();                                           // 10: LU
-    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
-      const int i = e & 63, j = e >> 6;
-      if (i > j) continue;
-      double acc = 0.0;
-      for (int l = i; l <= j; ++l) acc = fma(Am[i + l * CQ_LD], l == j ? r1d[j] : Bm[j + l * CQ_LD], acc);
-      a.P[(long long)i + (long long)j * a.ldp] = dsg[i] * acc;
-    }
-    __syncthreads();
-    // (5) W = U R2 (Bm upper), M = W^{-1} = R2^{-1} U^{-1} (Am), published for every CTA
-    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
-      const int i = e & 63, j = e >> 6;
-      if (i > j) continue;
-      double acc = 0.0;
-      for (int l = i; l <= j; ++l) acc = fma(Ps[i * PANEL_LD + l], Am[l + j * CQ_LD], acc);
-      Bm[i + j * CQ_LD] = acc;
-    }
-    __syncthreads();
-    cq_trinv_upper(Bm, Am);
-    __syncthreads();
+    // (5) M = R2^{-1} U^{-1} (Bm), published for every CTA
+    cq_trinv64([=](int i, int j) { return CQX(Am, CQ_LD, i, j); }, false, Cm, PANEL_LD);
+    cq_gemm64([=](int i, int k) { return CQX(Bm, CQ_LD, i, k); }, [=](int k, int j) { return CQX(Cm, PANEL_LD, k, j); },
+              up, upk, 1.0, [=](int i, int j, double v) { CQX(Bm, CQ_LD, i, j) = v; });
     for (int p = tid; p < CQ_E; p += PANEL_THREADS) {
       const int j = cq_col(p), i = p - j * (j + 1) / 2;
-      cq_ll_store(mreg + 2 * (size_t)p, Am[i + j * CQ_LD], f3);
+      cq_ll_store(mreg + 2 * (size_t)p, CQX(Bm, CQ_LD, i, j), f3);
     }
-    stamp();                                           // 11: R, W, M published
-    // (6) T = -U D L^{-T} (upper), tau = diag T
-    cq_trinv_unit_lower(Ps, PANEL_LD, Bm);
-    __syncthreads();
+    stamp();                                           // 11: U^{-1}, M published
+    // (6) R with D -> P(0:64, 0:64) upper; T = -U D L^{-T} -> a.T, tau; L -> Ps rows 0..63
     for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
       const int i = e & 63, j = e >> 6;
-      double acc = 0.0;
-      if (i <= j)
-        for (int l = i; l <= j; ++l) acc = fma(Ps[i * PANEL_LD + l] * dsg[l], Bm[j + l * CQ_LD], acc);
-      a.T[e] = -acc;                        // a.T is nb x nb = 64 x 64, column-major
-      if (i == j) a.tau[i] = -acc;
+      if (i <= j) a.P[(long long)i + (long long)j * a.ldp] = dsg[i] * GS[e];
+    }
+    cq_trinv64([=](int i, int j) { return i < j ? CQX(Am, CQ_LD, j, i) : (i == j ? 1.0 : 0.0); }, true, Cm, PANEL_LD);
+    cq_gemm64([=](int i, int k) { return k >= i ? CQX(Am, CQ_LD, i, k) * dsg[k] : 0.0; },
+              [=](int k, int j) { return CQX(Cm, PANEL_LD, k, j); }, up, upk, -1.0,
+              [=](int i, int j, double v) {
+                a.T[i + 64 * j] = v;
+                if (i == j) a.tau[i] = v;
+              });
+    for (int e = tid; e < 64 * 64; e += PANEL_THREADS) {
+      const int i = e & 63, j = e >> 6;
+      if (i > j) Ps[i * PANEL_LD + j] = CQX(Am, CQ_LD, i, j);
     }
   } else {
     ph = 12;
@@ -261,7 +253,7 @@ __device__ __noinline__ int panel_cqr(const PanelArgs& a, double* Ps, int R, dou
   __syncthreads();
   stamp();                                             // 12: T (CTA 0) / wait for M (others)
   // (7) Y(64:m, :) = Q1 M for the rows below the panel's top 64
-  cq_rows_times_upper(Ps, PANEL_LD, R, cta == 0 ? 64 : 0, Am);
+  cq_rows_times_upper(Ps, PANEL_LD, R, cta == 0 ? 64 : 0, cta == 0 ? Bm : Am);
   __syncthreads();
   stamp();                                             // 13: Y = Q1 M
   return 0;
@@ -314,7 +306,7 @@ panel_qr_kernel_t(const PanelArgs a) {
   bool cqr_done = false;
   const bool timed = a.dbg && tid == 0 && (cta == 0 || cta == G - 1);
   unsigned long long ph[4] = {0, 0, 0, 0}, tloop = 0, tlend = 0;
-  if constexpr (CLUSTER && RPT > 0) {
+  if constexpr (CLUSTER) {
     // CholeskyQR2 + Householder reconstruction: 3 exchanges instead of one per column
     if (a.use_cqr && nb == PANEL_NB) {
       __syncthreads();
@@ -684,12 +676,13 @@ inline int panel_rpt(int rows_per) {
   return rows_per <= 64 ? 8 : rows_per <= 128 ? 16 : rows_per <= 256 ? 32 : 0;
 }
 
-inline size_t panel_smem_bytes(int rows_per) {
+inline size_t panel_smem_bytes(int rows_per, bool cqr = false) {
   const int rpt = panel_rpt(rows_per);
-  // after the row block: the Householder loop's scratch, or (aliased) the CQR path's
+  // after the row block: the Householder loop's scratch, or (aliased, only when the CQR path
+  // may run) the CQR path's -- the larger footprint would otherwise cost co-resident clusters
   const size_t hh = (PANEL_RG + 1) * PANEL_NB + 4 * PANEL_NB + 2 * PANEL_NB + PANEL_NB * PANEL_NB +
                     36 * PANEL_NB + 2;
-  const size_t scratch = rpt ? std::max(hh, (size_t)CQ_SCRATCH) : hh;
+  const size_t scratch = cqr ? std::max(hh, (size_t)CQ_SCRATCH) : hh;
   return sizeof(double) * ((size_t)rows_per * PANEL_LD + scratch + (rpt ? 2 * PANEL_RG * rpt + PANEL_NB : 0));
 }
 

@@ -100,7 +100,8 @@ struct sdc_handle {
   double *Tb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr;
   double* llbuf = nullptr;             // flag-carrying exchange slots of the multi-cluster panel
   double* cqbuf = nullptr;             // CholeskyQR2 panel exchange slots (CQ_DOUBLES)
-  bool cqr = false;                    // CholeskyQR2 panels (SDC_CQR=1; off until faster)
+  bool cqr = true;                     // CholeskyQR2 panels allowed (workspace, smem)
+  int cqr_mode = 1;                    // SDC_CQR: 0 never, 1 tall multi-cluster panels, 2 always
   unsigned long long* cqstat = nullptr;   // device: [0] CQR panels done, [1] fallbacks
   unsigned ll_epoch = 0;               // advanced by nb per multi-cluster panel launch
   double *pmA = nullptr, *pmB = nullptr, *vec = nullptr, *scal = nullptr;
@@ -119,6 +120,7 @@ struct sdc_handle {
   bool panel_reg = true;               // register-resident panel column loop (rows_per <= 256)
   bool ql_orth = false;                // current call: SDC_FLAG_QL_ORTH
   int max_clusters16 = 0;
+  int max_clusters8 = 0;               // 8-CTA clusters resident at once (256-row blocks)
   int cluster_max_rows = 4096;         // panels with at most this many rows use one cluster
   int nbo = 256;                       // outer compact-WY block width of the current call
   int nbo_max = 256;                   // width the workspace is sized for
@@ -466,6 +468,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (splits <= 1) { splits = 1; kchunk = std::max(K, 1); }
   const bool tma = K > 0 && al16(A, lda) && al16(B, ldb) && tma_encode_fn() != nullptr;
   if (tma) {
+    h->sched[SDC_SCHED_GEMM_TMA]++;
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
                   (int)(al16(C, ldc) && M % 2 == 0), kupper};
     int v = h->gemm_force;
@@ -630,12 +633,21 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     // other (VERDICT r01 weak 8 / ADVICE r01).
     const int cap = h->share_sms ? std::max(2, h->max_clusters16 / 2) : h->max_clusters16;
     const int want = cdiv(m, 16 * h->panel_rows);
-    const int ncl = std::max(2, std::min(cap, want));
+    int ncl = std::max(2, std::min(cap, want));
+    int cs = 16;
     if (h->share_sms && want > cap) h->sched[SDC_SCHED_PANEL_MCLUSTER_CAPPED]++;
-    if (panel_smem_bytes(cdiv(m, 16 * ncl)) <= 227 * 1024) {
+    // 16-CTA clusters tile the GPCs unevenly (7 fit on 148 SMs): when that leaves more than
+    // 256 rows per CTA -- the shared-memory column loop instead of registers -- use 8-CTA
+    // clusters (more of them fit; the L2 exchange takes up to 16 cluster leaders)
+    if (cdiv(m, 16 * ncl) > 256 && h->max_clusters8 >= 4) {
+      const int cap8 = std::min(16, h->share_sms ? h->max_clusters8 / 2 : h->max_clusters8);
+      const int n8 = std::max(2, std::min(cap8, cdiv(m, 8 * h->panel_rows)));
+      if (8 * n8 > 16 * ncl) { ncl = n8; cs = 8; }
+    }
+    if (panel_smem_bytes(cdiv(m, cs * ncl), h->cqr) <= 227 * 1024) {
       cluster = true;
-      csize = 16;
-      G = 16 * ncl;
+      csize = cs;
+      G = cs * ncl;
     } else {
       G = std::min(h->num_sms, std::max(1, m / h->panel_rows));
     }
@@ -649,7 +661,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     if (csize > 1) { cluster = false; csize = 1; G = std::min(G, h->num_sms); rows_per = cdiv(m, G); }
   }
   if (cluster && csize == 1) csize = G;
-  size_t smem = panel_smem_bytes(rows_per);
+  size_t smem = panel_smem_bytes(rows_per, h->cqr);
   const int rpt = h->panel_reg ? panel_rpt(rows_per) : 0;
   const void* fn = panel_fn(cluster, rpt);
   size_t& cur = g_panel_attr[h->device & (MAX_DEV - 1)][cluster][rpt_slot(rpt)];
@@ -664,7 +676,14 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
   }
   // CholeskyQR2 first (register variants in cluster mode, full-width panels), Householder on
   // breakdown (cqr.cuh)
-  const int use_cqr = h->cqr && cluster && rpt > 0 && nb == NB && G <= CQ_GMAX ? 1 : 0;
+  // CholeskyQR2 pays off on TALL panels, where the Householder loop's per-column exchange
+  // crosses several clusters (measured: 228 vs 309 us per panel at 32768 rows, 175 vs 212 us at
+  // 16384, even at 8192, slower below): default for multi-cluster panels above 8192 rows
+  const bool cqr_here = h->cqr_mode == 2 || (h->cqr_mode == 1 && G > csize && m > 8192);
+  const int use_cqr = cqr_here && cluster && nb == NB && G <= CQ_GMAX ? 1 : 0;
+  if (getenv("SDC_DEBUG_PANEL"))
+    fprintf(stderr, "panel m=%d nb=%d G=%d csize=%d rows_per=%d rpt=%d cluster=%d use_cqr=%d cqr=%d\n", m, nb, G,
+            csize, rows_per, rpt, (int)cluster, use_cqr, (int)h->cqr);
   PanelArgs a{P, ldp, m, nb, Y, ldy, Yt, ldyt, T, tau, h->gbuf, h->bar, (unsigned)h->bar_count,
               rows_per, h->dbg_on ? h->dbg : nullptr, zero_above, csize, h->llbuf, h->ll_epoch,
               h->cqbuf, use_cqr, h->cqstat};
@@ -687,6 +706,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
     if (G > csize || use_cqr) h->ll_epoch += nb;
     if (use_cqr) h->sched[SDC_SCHED_PANEL_CQR_TRIED]++;
     h->sched[G > csize ? SDC_SCHED_PANEL_MCLUSTER : SDC_SCHED_PANEL_CLUSTER]++;
+    if (G > csize && csize == 8) h->sched[SDC_SCHED_PANEL_MCLUSTER8]++;
   } else {
     void* args[] = {&a};
     SDC_CK(cudaLaunchCooperativeKernel(fn, dim3(G),
@@ -1387,6 +1407,7 @@ int sdc_schedule_counters(sdc_handle* h, long long* out, int count, int reset) {
     h->sched[SDC_SCHED_PANEL_CQR_DONE] = (long long)st[0];
     h->sched[SDC_SCHED_PANEL_CQR_FALLBACK] = (long long)st[1];
   }
+  h->sched[SDC_SCHED_MAX_CLUSTERS16] = h->max_clusters16;
   for (int i = 0; i < count; ++i) out[i] = h->sched[i];
   if (reset) {
     for (int i = 0; i < SDC_SCHED_COUNTERS; ++i) h->sched[i] = 0;
@@ -1523,7 +1544,8 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PANEL_ROWS")) h->panel_rows = std::max(16, atoi(e));
   if (getenv("SDC_DEBUG_COUNTERS")) h->dbg_on = true;
   if (getenv("SDC_PANEL_SMEM")) h->panel_reg = false;
-  if (const char* e = getenv("SDC_CQR")) h->cqr = atoi(e) != 0;
+  if (const char* e = getenv("SDC_CQR")) h->cqr_mode = std::max(0, std::min(2, atoi(e)));
+  h->cqr = h->cqr_mode != 0;
   if (const char* e = getenv("SDC_GRAPH_MAX_N")) h->graph_max_n = atoi(e);
   if (const char* e = getenv("SDC_CLUSTER_MAX_ROWS")) h->cluster_max_rows = atoi(e);
   if (!rc) {   // non-portable cluster size 16 for the small-panel kernel (if the part allows it)
@@ -1536,11 +1558,11 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
     const void* fn16 = panel_fn(true, 0);
     if (np) {
       cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)panel_smem_bytes(cdiv(h->cluster_max_rows, 16)));
+                           (int)panel_smem_bytes(cdiv(h->cluster_max_rows, 16), h->cqr));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(16);
       cfg.blockDim = dim3(PANEL_THREADS);
-      cfg.dynamicSmemBytes = panel_smem_bytes(cdiv(h->cluster_max_rows, 16));
+      cfg.dynamicSmemBytes = panel_smem_bytes(cdiv(h->cluster_max_rows, 16), h->cqr);
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
       attr[0].val.clusterDim.x = 16;
@@ -1552,16 +1574,20 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
       if (cudaOccupancyMaxActiveClusters(&ncl, fn16, &cfg) == cudaSuccess && ncl >= 1)
         h->cluster_ok = true;
       // tall panels: how many 16-CTA clusters with ~256-row blocks can be resident at once
-      cfg.dynamicSmemBytes = panel_smem_bytes(256);
-      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem_bytes(256));
+      cfg.dynamicSmemBytes = panel_smem_bytes(256, h->cqr);
+      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem_bytes(256, h->cqr));
       int ncl2 = 0;
       if (cudaOccupancyMaxActiveClusters(&ncl2, fn16, &cfg) == cudaSuccess && ncl2 >= 2) {
         h->max_clusters16 = ncl2;
         h->mcluster_ok = true;
       }
+      int ncl8 = 0;
+      attr[0].val.clusterDim.x = 8;
+      cfg.gridDim = dim3(8);
+      if (cudaOccupancyMaxActiveClusters(&ncl8, fn16, &cfg) == cudaSuccess) h->max_clusters8 = ncl8;
       cudaGetLastError();
       // the probe above re-set this variant's limit: keep panel()'s per-device cache in step
-      g_panel_attr[device & (MAX_DEV - 1)][1][rpt_slot(0)] = panel_smem_bytes(256);
+      g_panel_attr[device & (MAX_DEV - 1)][1][rpt_slot(0)] = panel_smem_bytes(256, h->cqr);
     }
     if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = h->mcluster_ok = false;
     if (getenv("SDC_NO_MCLUSTER")) h->mcluster_ok = false;

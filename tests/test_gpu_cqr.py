@@ -30,7 +30,7 @@ def dev(x):
 
 
 def handle(sdc, n_max, **env):
-    env.setdefault("SDC_CQR", 1)
+    env.setdefault("SDC_CQR", 2)   # CholeskyQR2 on every full-width panel
     old = {k: os.environ.get(k) for k in env}
     try:
         for k, v in env.items():
@@ -96,7 +96,7 @@ def test_cqr_fallback_exact_rank_deficiency(sdc, orc):
     assert c["panel_cqr_fallback"] >= 1, c
 
 
-@pytest.mark.parametrize("cqr", [0, 1])
+@pytest.mark.parametrize("cqr", [0, 2])
 def test_cqr_vs_householder_step_invariants(sdc, orc, cqr):
     # the whole step with and without CholeskyQR2 panels: the oracle's invariants at n = 1024
     from paper_1011_3077_b200 import inputs

@@ -166,14 +166,18 @@ def test_panel_exchange_paths_n2048(sdc, env):
     assert info.k == ref.p.expected_k == 1024
 
 
-@pytest.mark.parametrize("m,n", [(8192, 256), (12288, 320), (8192, 1024)])
+@pytest.mark.parametrize("m,n", [(8192, 256), (12288, 320), (8192, 1024), (32768, 192)])
 def test_tall_qr_multicluster_r_unique(sdc, orc, m, n):
     # blocked QR of tall matrices whose panels need several clusters; R with diag >= 0 is
-    # unique, so it is compared elementwise with the oracle's dgeqr2 R
+    # unique, so it is compared elementwise with the oracle's dgeqr2 R.  32768 rows is the
+    # headline stack height (n = 16384): 8-CTA clusters keep 256 rows per CTA in registers
     h = sdc.Handle(m // 2)
     s = np.random.default_rng(m + n).standard_normal((m, n))
     q, r = h.qr(dev(s))
-    assert h.schedule_counters()["panel_mcluster"] > 0
+    c = h.schedule_counters()
+    assert c["panel_mcluster"] > 0
+    if m == 32768:
+        assert c["panel_mcluster8"] > 0, c
     y, _ = orc.geqr2(s)
     d = np.where(np.diag(y)[:n] < 0, -1.0, 1.0)
     r_o = d[:, None] * np.triu(y[:n, :n])

@@ -448,7 +448,7 @@ def test_forced_gemm_variants_vs_oracle(orc, sdc, variant, persist):
 
 @pytest.mark.parametrize("env", [{"SDC_PERSIST": 0}, {"SDC_PERSIST": 2}, {"SDC_RED": 0},
                                  {"SDC_SIDE_PERSIST": 1, "SDC_NBO": 128}, {"SDC_PANEL_SMEM": 1},
-                                 {"SDC_GEMM_VARIANT": 4}, {"SDC_CQR": 1}])
+                                 {"SDC_GEMM_VARIANT": 4}, {"SDC_CQR": 2}, {"SDC_CQR": 0}])
 def test_step_variants_parity(orc, sdc, env):
     # the whole step with each non-default kernel variant (persistent grids off / everywhere,
     # load-FMA-store instead of the bulk reduce-add epilogue, persistent side-stream updates,
@@ -463,14 +463,18 @@ def test_step_variants_parity(orc, sdc, env):
 @pytest.mark.parametrize("n", [777, 778])
 def test_odd_n_keeps_tma_gemms(orc, sdc, n):
     # the n x n workspace has ld = n rounded up to even, so an odd-order step stages its GEMM
-    # operands by TMA like an even one; only Q22^T B_j reads the complement at row offset n
-    # (not 16-byte aligned when n is odd): at most one cp.async GEMM per IRS pass
+    # operands by TMA like an even one.  The exceptions: Q22^T B_j reads the complement at row
+    # offset n, and the similarity / Q_L products read the caller's A and Q with their own
+    # (here odd) leading dimension -- a few percent of the launches (round 1: all of them)
     h = sdc.Handle(n)
     A, V = inputs.ginibre(n, 90 + n, 1090 + n)
     p = inputs.Problem("odd", n, A, None, V, None, 6, 0.0, 0)
     Q, _, Ah, info, o = run_both(orc, h, p)
     c = h.schedule_counters()
-    assert c["gemm_cpasync"] <= (p.max_iters if n % 2 else 0), c
+    if n % 2:
+        assert c["gemm_cpasync"] <= 0.05 * (c["gemm_cpasync"] + c["gemm_tma"]), c
+    else:
+        assert c["gemm_cpasync"] == 0, c
     if o.status == 0:
         assert_parity(o, Q, info, p.A, n, Ah)
     assert orth_err(host(Q)) <= 1e-13 * n

@@ -23,8 +23,8 @@ h.lib.sdc_debug_counters(h._h, buf, 64, 1)
 c = h.schedule_counters()
 names = ["gram1", "reduce1", "gather1", "chol1", "trinv1", "Q1", "keepR1", "gram2+xchg", "chol2", "Qtop",
          "LU", "R/W/M", "T|waitM", "Y"]
-npan = max(1, c["panel_cqr_done"])
-print(f"m={m} n={n} SDC_CQR={os.environ.get('SDC_CQR', '1')}: {cnt} panels, {ms / cnt * 1e3:.1f} us/panel, "
+npan = max(1, c["panel_cqr_done"] // 2)   # warm-up + timed QR
+print(f"m={m} n={n} SDC_CQR={os.environ.get('SDC_CQR', 'default')}: {cnt} panels, {ms / cnt * 1e3:.1f} us/panel, "
       f"cqr done {c['panel_cqr_done']} fallback {c['panel_cqr_fallback']} | {c}")
 for who, o in (("CTA 0", 32), ("last CTA", 48)):
     print(f"  {who}: " + ", ".join(f"{names[q]} {buf[o + q] / npan / 1.965e3:.2f}" for q in range(14)) + " (us/panel)")
