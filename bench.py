@@ -309,7 +309,7 @@ def run_schur(args, rank, world, local):
     import torch.distributed as dist
     from paper_1011_3077_b200 import api, inputs
     n = args.n or 4096
-    leaf = 64
+    leaf = args.leaf
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -530,6 +530,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-n", type=int, default=1536)
+    ap.add_argument("--leaf", type=int, default=64,
+                    help="config 8: largest diagonal block left unsplit (1 = down to 1x1 / 2x2 blocks; blocks of "
+                         "order <= 64 run in the batched kernel)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))

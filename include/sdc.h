@@ -340,7 +340,14 @@ enum { SDC_SCHED_LOOKAHEAD_FORKS = 0,  /* look-ahead QR schedules forked to the 
        SDC_SCHED_PANEL_MCLUSTER8 = 14, /* multi-cluster panels built from 8-CTA clusters (tall
                                           stacks: keeps <= 256 rows per CTA in registers)    */
        SDC_SCHED_GEMM_TMA = 15,        /* step GEMMs staged by TMA                              */
-       SDC_SCHED_COUNTERS = 16 };
+       SDC_SCHED_SCHUR_BATCH_LAUNCHES = 16, /* sdc_schur: launches of the batched small-block
+                                          kernel (one per recursion level and size class)   */
+       SDC_SCHED_SCHUR_BATCH_BLOCKS = 17,   /* ... diagonal blocks (order <= 64) they processed */
+       SDC_SCHED_PANEL_CQ_SPLIT = 18,  /* panels factored by the split CholeskyQR2 kernel chain
+                                          (tall stack panels next to the bulk update)         */
+       SDC_SCHED_CQ_SPLIT_BREAKDOWNS = 19, /* ... whose Cholesky broke down (fallback kernel ran;
+                                          known after the call's final synchronisation)       */
+       SDC_SCHED_COUNTERS = 20 };
 /* Copies `count` (<= SDC_SCHED_COUNTERS) counters to the HOST array out; reset != 0 zeroes
  * them.  count > SDC_SCHED_PANEL_CQR_DONE synchronises the device (device-side counters).
  * Returns 0, -1 (null handle), -3 (bad count) or -100. */

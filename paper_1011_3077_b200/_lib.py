@@ -16,7 +16,8 @@ SPLIT_ACCEPT = 1e-8
 SCHED_NAMES = ("lookahead_forks", "xpass_forks", "ctx_forks", "panel_cluster", "panel_mcluster",
                "panel_grid", "graph_captures", "graph_replays", "panel_mcluster_capped", "panel_cqr_tried",
                "panel_cqr_done", "panel_cqr_fallback", "gemm_cpasync", "max_clusters16",
-               "panel_mcluster8", "gemm_tma")
+               "panel_mcluster8", "gemm_tma", "schur_batch_launches", "schur_batch_blocks",
+               "panel_cq_split", "cq_split_breakdowns")
 
 
 class SdcResult(ctypes.Structure):

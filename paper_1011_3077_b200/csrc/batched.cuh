@@ -167,106 +167,124 @@ SDC_DEV void bq_qr(int m, int n, int np, double* P, int ldp, double* T, int tld,
   }
 }
 
-__global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArgs a) {
-  extern __shared__ __align__(16) double smq[];
-  const int n = a.n, m = 2 * n, b = blockIdx.x, tid = threadIdx.x;
-  // leading dimensions = 4 (mod 16) doubles: the DMMA fragment loads (8 rows x 4 k of one
-  // operand per instruction) and the T column loop hit 16 distinct bank pairs per half-warp
-  const int np = (n + 15) & ~15, ld = np + 4, NL = ld * np, ldp = 2 * np + 4;
-  double* Aj = smq;                 // np x np (ld)
-  double* Bj = Aj + NL;
-  double* P = Bj + NL;              // 2np x np (ldp): stack / factored matrices
-  double* T = P + (size_t)ldp * np; // np x np (ld); W aliases T (T is dead whenever W is live)
-  double* W = T;
-  double* Z = T + NL;
-  double* sc = Z + NL;              // np
-  double* beta = sc + np;
-  double* g = beta + np;            // np
-  double* msel = g + np;            // np
-  double* red = msel + np;          // 2 * BAT_WARPS + 16
-  const double* A0 = a.A + (long long)b * a.sa;
-  const double* V0 = a.V + (long long)b * a.sv;
-
-  for (int e = tid; e < np * np; e += BQ_THREADS) {
-    const int i = e % np, j = e / np;
-    const bool in = i < n && j < n;
-    Aj[i + j * ld] = in ? A0[i + (long long)j * a.lda] : 0.0;
-    Bj[i + j * ld] = (in && i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  double nA = 0.0, fA;
-  {
-    double f = 0.0;
-    for (int e = tid; e < np * np; e += BQ_THREADS) { const double v = Aj[e % np + (e / np) * ld]; f += v * v; }
-    fA = sqrt(bat_sum(f, red));
-    if (tid < n) {
-      double c = 0.0;
-      for (int i = 0; i < n; ++i) c += fabs(Aj[i + tid * ld]);
-      msel[tid] = c;
-    }
-    __syncthreads();
-    for (int j = 0; j < n; ++j) nA = fmax(nA, msel[j]);
-    __syncthreads();
-  }
+// Shared-memory layout of one problem of order n (np = n rounded up to 16).  Leading
+// dimensions = 4 (mod 16) doubles: the DMMA fragment loads (8 rows x 4 k of one operand per
+// instruction) and the T column loop hit 16 distinct bank pairs per half-warp.
+struct BqSm {
+  int n, np, ld, NL, ldp;
+  double *Aj, *Bj;        // np x np (ld): A_j, B_j; after bq_split_tail: Ahat, Q
+  double* P;              // 2np x np (ldp): stack / factored matrices
+  double *T, *W, *Z;      // np x np (ld); W aliases T (T is dead whenever W is live)
+  double *sc, *beta, *g, *msel, *red;
   // implicit unit-lower Y of the last factorisation of P (rows m_, columns n)
-  auto Yv = [&](int r, int k, int m_) -> double {
+  SDC_DEV double Yv(int r, int k, int m_) const {
     if (k >= n || r >= m_ || r < k) return 0.0;
     return r == k ? 1.0 : sc[k] * P[r + k * ldp];
-  };
-
-  // ---- IRS passes (Alg. 3) -----------------------------------------------------------
-  for (int pass = 0; pass < a.passes; ++pass) {
-    for (int e = tid; e < ldp * np; e += BQ_THREADS) {   // P = [B_j; -A_j] (rows >= 2n zero)
-      const int i = e % ldp, j = e / ldp;
-      double v = 0.0;
-      if (j < n) v = i < n ? Bj[i + j * ld] : (i < m ? -Aj[(i - n) + j * ld] : 0.0);
-      P[e] = v;
-    }
-    __syncthreads();
-    bq_qr(m, n, np, P, ldp, T, ld, sc, beta, g, msel);
-    // Z = T Y2^T  (T dead afterwards: W may overwrite it)
-    bq_mma(np, np, np, [&](int i, int k) { return T[i + k * ld]; },
-           [&](int k, int j) { return Yv(n + j, k, m); },
-           [&](int i, int j, double v) { Z[i + j * ld] = v; });
-    // W = Y1^T A_j ;  A_{j+1} = -Z^T W
-    bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
-           [&](int k, int j) { return Aj[k + j * ld]; },
-           [&](int i, int j, double v) { W[i + j * ld] = v; });
-    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
-           [&](int k, int j) { return W[k + j * ld]; },
-           [&](int i, int j, double v) { Aj[i + j * ld] = -v; });
-    // W = Y2^T B_j ;  B_{j+1} = B_j - Z^T W
-    bq_mma(np, np, np, [&](int i, int k) { return Yv(n + k, i, m); },
-           [&](int k, int j) { return Bj[k + j * ld]; },
-           [&](int i, int j, double v) { W[i + j * ld] = v; });
-    bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
-           [&](int k, int j) { return W[k + j * ld]; },
-           [&](int i, int j, double v) { Bj[i + j * ld] -= v; });
   }
+};
 
-  // ---- GRURV(2, A_p + B_p, A_p; -1, +1) ------------------------------------------------
+SDC_DEV BqSm bq_carve(double* smq, int n) {
+  BqSm s;
+  s.n = n;
+  s.np = (n + 15) & ~15;
+  s.ld = s.np + 4;
+  s.NL = s.ld * s.np;
+  s.ldp = 2 * s.np + 4;
+  s.Aj = smq;
+  s.Bj = s.Aj + s.NL;
+  s.P = s.Bj + s.NL;
+  s.T = s.P + (size_t)s.ldp * s.np;
+  s.W = s.T;
+  s.Z = s.T + s.NL;
+  s.sc = s.Z + s.NL;
+  s.beta = s.sc + s.np;
+  s.g = s.beta + s.np;
+  s.msel = s.g + s.np;
+  s.red = s.msel + s.np;   // 2 * BAT_WARPS + 16
+  return s;
+}
+
+// one IRS pass (Alg. 3 l.3): (A_j, B_j) -> (A_{j+1}, B_{j+1}) in place
+SDC_DEV void bq_irs_pass(const BqSm& s) {
+  const int n = s.n, m = 2 * n, np = s.np, ld = s.ld, ldp = s.ldp, tid = threadIdx.x;
+  double *Aj = s.Aj, *Bj = s.Bj, *P = s.P, *T = s.T, *W = s.W, *Z = s.Z;
+  for (int e = tid; e < ldp * np; e += BQ_THREADS) {   // P = [B_j; -A_j] (rows >= 2n zero)
+    const int i = e % ldp, j = e / ldp;
+    double v = 0.0;
+    if (j < n) v = i < n ? Bj[i + j * ld] : (i < m ? -Aj[(i - n) + j * ld] : 0.0);
+    P[e] = v;
+  }
+  __syncthreads();
+  bq_qr(m, n, np, P, ldp, T, ld, s.sc, s.beta, s.g, s.msel);
+  // Z = T Y2^T  (T dead afterwards: W may overwrite it)
+  bq_mma(np, np, np, [&](int i, int k) { return T[i + k * ld]; },
+         [&](int k, int j) { return s.Yv(n + j, k, m); },
+         [&](int i, int j, double v) { Z[i + j * ld] = v; });
+  // W = Y1^T A_j ;  A_{j+1} = -Z^T W
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(k, i, n); },
+         [&](int k, int j) { return Aj[k + j * ld]; },
+         [&](int i, int j, double v) { W[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
+         [&](int k, int j) { return W[k + j * ld]; },
+         [&](int i, int j, double v) { Aj[i + j * ld] = -v; });
+  // W = Y2^T B_j ;  B_{j+1} = B_j - Z^T W
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(n + k, i, m); },
+         [&](int k, int j) { return Bj[k + j * ld]; },
+         [&](int i, int j, double v) { W[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Z[k + i * ld]; },
+         [&](int k, int j) { return W[k + j * ld]; },
+         [&](int i, int j, double v) { Bj[i + j * ld] -= v; });
+}
+
+// Explicit Q of the last bq_qr of an n x n P with the columns scaled by sign(R_jj):
+// out(i, j) = sign(beta[j]) (I - (Y T) Y^T)(i, j)   (the Haar factor of a Gaussian P)
+template <class FO>
+SDC_DEV void bq_form_q_signed(const BqSm& s, FO out) {
+  const int n = s.n, np = s.np, ld = s.ld;
+  double *T = s.T, *W = s.W, *Z = s.Z;
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(i, k, n); },
+         [&](int k, int j) { return T[k + j * ld]; },
+         [&](int i, int j, double v) { Z[i + j * ld] = v; });
+  bq_mma(np, np, np, [&](int i, int k) { return Z[i + k * ld]; },
+         [&](int k, int j) { return s.Yv(j, k, n); },
+         [&](int i, int j, double v) { W[i + j * ld] = (i == j && i < n ? 1.0 : 0.0) - v; });
+  for (int e = threadIdx.x; e < n * n; e += BQ_THREADS) {
+    const int i = e % n, j = e / n;
+    out(i, j, (s.beta[j] < 0.0 ? -1.0 : 1.0) * W[i + j * ld]);
+  }
+  __syncthreads();
+}
+
+// GRURV(2, A_p + B_p, A_p; -1, +1) with the Haar V0, similarity with the original A0 and the
+// split selection.  In: Aj = A_p, Bj = B_p (destroyed).  Out: Bj = Q, Aj = Ahat = Q^T A0 Q,
+// red[2 BAT_WARPS] = r, red[2 BAT_WARPS + 1] = min_r ||Ahat(r:, :r)||_1 / nA (ties: smallest r).
+SDC_DEV void bq_split_tail(const BqSm& s, const double* A0, long long lda, const double* V0,
+                           long long ldv, double nA) {
+  const int n = s.n, np = s.np, ld = s.ld, ldp = s.ldp, tid = threadIdx.x;
+  double *Aj = s.Aj, *Bj = s.Bj, *P = s.P, *T = s.T, *W = s.W, *Z = s.Z;
+  double *beta = s.beta, *msel = s.msel, *red = s.red;
   // X = A_p V^T into P (ld 2np)
   bq_mma(np, np, np, [&](int i, int k) { return Aj[i + k * ld]; },
-         [&](int k, int j) { return (k < n && j < n) ? V0[j + (long long)k * a.ldv] : 0.0; },
+         [&](int k, int j) { return (k < n && j < n) ? V0[j + (long long)k * ldv] : 0.0; },
          [&](int i, int j, double v) { P[i + j * ldp] = v; });
-  bq_qr(n, n, np, P, ldp, T, ld, sc, beta, g, msel);                    // X = U R_2
+  bq_qr(n, n, np, P, ldp, T, ld, s.sc, beta, s.g, msel);               // X = U R_2
   for (int e = tid; e < np * np; e += BQ_THREADS) {                   // S = A_p + B_p
     const int i = e % np, j = e / np;
     Aj[i + j * ld] += Bj[i + j * ld];
   }
   __syncthreads();
   // U^T S = S - (Y T^T)(Y^T S):  Z = Y T^T (last use of T), W = Y^T S, S -= Z W, row signs
-  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(i, k, n); },
          [&](int k, int j) { return T[j + k * ld]; },
          [&](int i, int j, double v) { Z[i + j * ld] = v; });
-  bq_mma(np, np, np, [&](int i, int k) { return Yv(k, i, n); },
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(k, i, n); },
          [&](int k, int j) { return Aj[k + j * ld]; },
          [&](int i, int j, double v) { W[i + j * ld] = v; });
   bq_mma(np, np, np, [&](int i, int k) { return Z[i + k * ld]; },
          [&](int k, int j) { return W[k + j * ld]; },
          [&](int i, int j, double v) {
-           const double s = Aj[i + j * ld] - v;
-           Aj[i + j * ld] = (i < n && beta[i] < 0.0) ? -s : s;     // U <- U D_U
+           const double t = Aj[i + j * ld] - v;
+           Aj[i + j * ld] = (i < n && beta[i] < 0.0) ? -t : t;     // U <- U D_U
          });
   // M = C^T J into P: M(i, j) = C(n-1-j, i)
   for (int e = tid; e < ldp * np; e += BQ_THREADS) {
@@ -274,13 +292,13 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
     P[e] = (i < n && j < n) ? Aj[(n - 1 - j) + i * ld] : 0.0;
   }
   __syncthreads();
-  bq_qr(n, n, np, P, ldp, T, ld, sc, beta, g, msel);
+  bq_qr(n, n, np, P, ldp, T, ld, s.sc, beta, s.g, msel);
   // Q_qr = I - (Y T) Y^T:  Z = Y T (last use of T), W = I - Z Y^T
-  bq_mma(np, np, np, [&](int i, int k) { return Yv(i, k, n); },
+  bq_mma(np, np, np, [&](int i, int k) { return s.Yv(i, k, n); },
          [&](int k, int j) { return T[k + j * ld]; },
          [&](int i, int j, double v) { Z[i + j * ld] = v; });
   bq_mma(np, np, np, [&](int i, int k) { return Z[i + k * ld]; },
-         [&](int k, int j) { return Yv(j, k, n); },
+         [&](int k, int j) { return s.Yv(j, k, n); },
          [&](int i, int j, double v) { W[i + j * ld] = (i == j && i < n ? 1.0 : 0.0) - v; });
   // Q(:, j) = sign(R(jj, jj)) Q_qr(:, jj), jj = n-1-j  -> Bj
   for (int e = tid; e < np * np; e += BQ_THREADS) {
@@ -295,7 +313,7 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
   __syncthreads();
 
   // ---- similarity Ahat = Q^T A Q (original A), split selection ------------------------------
-  bq_mma(np, np, np, [&](int i, int k) { return (i < n && k < n) ? A0[i + (long long)k * a.lda] : 0.0; },
+  bq_mma(np, np, np, [&](int i, int k) { return (i < n && k < n) ? A0[i + (long long)k * lda] : 0.0; },
          [&](int k, int j) { return Bj[k + j * ld]; },
          [&](int i, int j, double v) { W[i + j * ld] = v; });
   bq_mma(np, np, np, [&](int i, int k) { return Bj[k + i * ld]; },
@@ -303,10 +321,10 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
          [&](int i, int j, double v) { Aj[i + j * ld] = v; });
   // suffix column sums: Z[c + r ld] = sum_{i >= r} |Ahat(i, c)| for c < r
   if (tid < n) {
-    double s = 0.0;
+    double t = 0.0;
     for (int r = n - 1; r >= 1; --r) {
-      s += fabs(Aj[r + tid * ld]);
-      Z[tid + r * ld] = s;
+      t += fabs(Aj[r + tid * ld]);
+      Z[tid + r * ld] = t;
     }
   }
   __syncthreads();
@@ -328,6 +346,47 @@ __global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArg
     red[2 * BAT_WARPS + 1] = msel[best];
   }
   __syncthreads();
+}
+
+// ||A||_1 (max column sum) and ||A||_F of the n x n matrix in Aj (uses msel, red)
+SDC_DEV void bq_norms(const BqSm& s, const double* X, double& n1, double& nf) {
+  const int n = s.n, np = s.np, ld = s.ld, tid = threadIdx.x;
+  double f = 0.0;
+  for (int e = tid; e < np * np; e += BQ_THREADS) { const double v = X[e % np + (e / np) * ld]; f += v * v; }
+  nf = sqrt(bat_sum(f, s.red));
+  if (tid < n) {
+    double c = 0.0;
+    for (int i = 0; i < n; ++i) c += fabs(X[i + tid * ld]);
+    s.msel[tid] = c;
+  }
+  __syncthreads();
+  n1 = 0.0;
+  for (int j = 0; j < n; ++j) n1 = fmax(n1, s.msel[j]);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BQ_THREADS, 1) k_split_batched_wy(const BatArgs a) {
+  extern __shared__ __align__(16) double smq[];
+  const int n = a.n, b = blockIdx.x, tid = threadIdx.x;
+  const BqSm s = bq_carve(smq, n);
+  const int np = s.np, ld = s.ld;
+  double *Aj = s.Aj, *Bj = s.Bj, *red = s.red;
+  const double* A0 = a.A + (long long)b * a.sa;
+  const double* V0 = a.V + (long long)b * a.sv;
+
+  for (int e = tid; e < np * np; e += BQ_THREADS) {
+    const int i = e % np, j = e / np;
+    const bool in = i < n && j < n;
+    Aj[i + j * ld] = in ? A0[i + (long long)j * a.lda] : 0.0;
+    Bj[i + j * ld] = (in && i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  double nA, fA;
+  bq_norms(s, Aj, nA, fA);
+
+  for (int pass = 0; pass < a.passes; ++pass) bq_irs_pass(s);          // IRS (Alg. 3)
+  bq_split_tail(s, A0, a.lda, V0, a.ldv, nA);                          // GRURV, similarity, selection
+
   const int rbest = (int)red[2 * BAT_WARPS];
   double f = 0.0, nf = 0.0;
   for (int e = tid; e < np * np; e += BQ_THREADS) {

@@ -32,6 +32,8 @@
 #include "panel.cuh"
 #include "trevc.cuh"
 #include "batched.cuh"
+#include "schur_batched.cuh"
+#include "cqr_split.cuh"
 
 using namespace sdc;
 
@@ -141,6 +143,18 @@ struct sdc_handle {
   // persistent grids on the side stream / second chain too
   int persist_mode = 1, red_mode = 1;
   bool side_persist = false;
+  // CholeskyQR2 panel as a chain of small kernels (cqr_split.cuh): SDC_CQ_SPLIT 0 never, 1 tall
+  // panels (> cq_split_rows rows) of the look-ahead stack QR of an IRS pass, 2 every full-width
+  // panel of >= 128 rows (tests).  cq_split_ctx: inside such a QR.  A reported breakdown turns
+  // mode 1 off for the handle (the fallback is correct but slow).
+  int cq_split = 1, cq_split_rows = 8192;
+  bool cq_split_ctx = false;
+  double* cqs = nullptr;
+  unsigned* cqs_sync = nullptr;
+  bool schur_batch = true;             // SDC_SCHUR_BATCH: blocks of order <= 64 of the recursion in
+                                       // one launch per level (schur_batched.cuh)
+  int upd_tile = 0;                    // SDC_UPD_TILE: 1 = 128x128 reduce-add update tiles (1 CTA/SM)
+  double split_eff = 0.9;              // SDC_SPLIT_EFF: wanted last-wave fill of split-K grids
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
   double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
@@ -195,7 +209,7 @@ struct sdc_handle {
   int gemm_sub = SDC_PROF_GEMM_OTHER;   // sub-class of the GEMMs being launched
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  struct ProfRec { int cls; int e0, e1; double work; };
+  struct ProfRec { int cls; int e0, e1; double work; int tag; };
   std::vector<ProfRec> recs;
   double prof_ms[SDC_PROF_CLASSES] = {0}, prof_work[SDC_PROF_CLASSES] = {0};
   long long prof_n[SDC_PROF_CLASSES] = {0};
@@ -281,8 +295,9 @@ struct ProfScope {
     if (h->prof_on && e0 >= 0) {
       int e1 = prof_event(h);
       if (e1 >= 0) {
-        h->recs.push_back({cls, e0, e1, work});
-        if (sub >= 0) h->recs.push_back({sub, e0, e1, work});
+        const int tag = (h->st == h->st_hi ? 1 : 0) | (h->on_side ? 2 : 0);   // stream of the launch
+        h->recs.push_back({cls, e0, e1, work, tag});
+        if (sub >= 0) h->recs.push_back({sub, e0, e1, work, tag});
       }
     }
   }
@@ -295,10 +310,13 @@ void prof_collect(sdc_handle* h) {
   for (auto& r : h->recs) cudaEventSynchronize(h->ev_pool[r.e1]);   // events on several streams
   const cudaEvent_t ref = h->ev_pool[h->recs.front().e0];
   std::vector<std::pair<float, float>> iv[SDC_PROF_CLASSES];
+  FILE* dump = nullptr;   // SDC_PROF_DUMP=path: one line per launch record (class, start, end in ms, work)
+  if (const char* dp = getenv("SDC_PROF_DUMP")) dump = fopen(dp, "a");
   for (auto& r : h->recs) {
     float a = 0.f, b = 0.f;
     cudaEventElapsedTime(&a, ref, h->ev_pool[r.e0]);
     cudaEventElapsedTime(&b, ref, h->ev_pool[r.e1]);
+    if (dump) fprintf(dump, "%d %d %.4f %.4f %.6g\n", r.cls, r.tag, a, b, r.work);
     iv[r.cls].push_back({a, b});
     h->prof_work[r.cls] += r.work;
     h->prof_n[r.cls] += 1;
@@ -315,6 +333,7 @@ void prof_collect(sdc_handle* h) {
     tot += hi - lo;
     h->prof_ms[c] += tot;
   }
+  if (dump) fclose(dump);
   h->recs.clear();
   h->ev_used = 0;
 }
@@ -335,6 +354,7 @@ using TmaS = TmaTile<64, 64, 32, 32, 6>;        // small grids, 4 consumer warps
 using TmaU = TmaTile<128, 64, 64, 32, 4, 2>;    // rank-nb updates: 2 CTAs/SM, epilogue overlap
 using TmaC = TmaTile<128, 128, 64, 32, 3, 1, true>;  // K <= 256 updates, C tile prefetched by TMA
 using TmaR = TmaTile<128, 64, 64, 32, 3, 2, false, true>;  // updates with beta = 1: bulk reduce-add
+using TmaR2 = TmaTile<128, 128, 64, 32, 4, 1, false, true>;  // same, 128x128 tiles, 1 CTA/SM
 
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
@@ -486,9 +506,11 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
     // would hold every SM until the whole update finished, and the critical chain's kernels
     // (panels, next-block updates, reductions) on the high-priority stream would queue
     // behind it; one-tile CTAs retire continuously, so the scheduler can hand SMs to them.
+    const bool big = h->upd_tile == 1 && M >= 1024 && N >= 1024;
     if (v == 3 && (h->on_side || h->two_chains) && !h->side_persist) {
       if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
-        return launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
+        return big ? launch_tma_t<TmaR2>(h, A, lda, B, ldb, g, splits)
+                   : launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
       return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
     }
     if (pm == 2 || (pm == 1 && v == 3)) {
@@ -498,7 +520,8 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
         case 2: return launch_tma_persist<TmaS>(h, A, lda, B, ldb, g, splits);
         case 3:
           if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
-            return launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
+            return big ? launch_tma_persist<TmaR2>(h, A, lda, B, ldb, g, splits)
+                       : launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
           return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
         default: break;
       }
@@ -539,7 +562,7 @@ int pick_splits(sdc_handle* h, int tiles, int K, long long cap) {
     const long long ctas = (long long)tiles * s;
     const long long waves = (ctas + P - 1) / P;
     const double eff = (double)ctas / (double)(waves * P);
-    if (ctas >= 2LL * P && eff >= 0.9) return s;
+    if (ctas >= 2LL * P && eff >= h->split_eff) return s;
     if (eff > best_eff + 1e-9 || (ctas < 2LL * P && s == smax)) { best_eff = eff; best = s; }
   }
   return best;
@@ -616,8 +639,41 @@ inline int rpt_slot(int rpt) { return rpt == 8 ? 1 : rpt == 16 ? 2 : rpt == 32 ?
 // kernel (the attribute is per device; sdc_create re-sets the cluster RPT=0 entry it probes)
 size_t g_panel_attr[MAX_DEV][2][4] = {};
 
+// The CholeskyQR2 panel as six small kernels (cqr_split.cuh): wide, bandwidth-trivial stages
+// on m/256 CTAs and the serial 64 x 64 chains on one CTA, so a tall panel that runs next to the
+// bulk trailing update holds one SM instead of 120 for most of its ~200 us.
+int panel_split(sdc_handle* h, double* P, long long ldp, int m, double* Y, long long ldy, double* Yt,
+                long long ldyt, double* T, double* tau, int zero_above) {
+  static DevOnce attr;
+  if (!attr.has(h->device)) {
+    SDC_CK(cudaFuncSetAttribute(k_cqs_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQS_WIDE_SMEM));
+    SDC_CK(cudaFuncSetAttribute(k_cqs_q1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQS_WIDE_SMEM));
+    SDC_CK(cudaFuncSetAttribute(k_cqs_y, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQS_WIDE_SMEM));
+    SDC_CK(cudaFuncSetAttribute(k_cqs_mid1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQS_MID_SMEM));
+    SDC_CK(cudaFuncSetAttribute(k_cqs_mid2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CQS_MID_SMEM));
+    attr.set(h->device);
+  }
+  const int G = cdiv(m, CQS_ROWS);
+  CqsArgs a{P, ldp, m, Y, ldy, Yt, ldyt, T, tau, zero_above, h->cqs, h->cqs_sync};
+  ProfScope ps(h, SDC_PROF_PANEL, 8.0 * 4.0 * m * NB);
+  k_cqs_gram<<<G, 512, CQS_WIDE_SMEM, h->st>>>(a);
+  k_cqs_mid1<<<CQS_MIDS, 512, CQS_MID_SMEM, h->st>>>(a, G);
+  k_cqs_q1<<<G, 512, CQS_WIDE_SMEM, h->st>>>(a);
+  k_cqs_mid2<<<CQS_MIDS, 512, CQS_MID_SMEM, h->st>>>(a, G);
+  k_cqs_y<<<G, 512, CQS_WIDE_SMEM, h->st>>>(a);
+  k_cqs_fallback<<<1, BQ_THREADS, CQS_FB_SMEM, h->st>>>(a);
+  SDC_CK(cudaGetLastError());
+  h->launches += 6;
+  h->sched[SDC_SCHED_PANEL_CQ_SPLIT]++;
+  return 0;
+}
+
 int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, long long ldy,
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
+  if (nb == NB && h->cqs && m <= CQS_GMAX * CQS_ROWS &&
+      (h->cq_split == 2 ? m >= 128
+                        : (h->cq_split == 1 && h->cq_split_ctx && m > h->cq_split_rows && !h->share_sms)))
+    return panel_split(h, P, ldp, m, Y, ldy, Yt, ldyt, T, tau, zero_above);
   // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange); taller panels: several
   // 16-CTA clusters with a two-level exchange (DSMEM inside, L2 between cluster leaders);
   // otherwise a cooperative grid exchanging through L2
@@ -963,7 +1019,17 @@ int irs_pass(sdc_handle* h, int n, const double* Aj, long long lda, const double
   Nvtx nv("irs_pass (Alg. 3 l.3)");
   const long long m = 2LL * n;
   const Fac f = fac_stack(h, n);
-  SDC_TRY(blocked_qr(h, S, m, (int)m, n, f));
+  {
+    // the stack [B_j; -A_j] has full column rank (R_j = chol(A_j^T A_j + B_j^T B_j)): its tall
+    // panels may run as the split CholeskyQR2 chain (GRURV's operands are rank-deficient by
+    // construction and keep the cluster kernel with its in-kernel Householder fallback)
+    struct SplitCtx {
+      sdc_handle* h; bool prev;
+      explicit SplitCtx(sdc_handle* h_) : h(h_), prev(h_->cq_split_ctx) { h->cq_split_ctx = true; }
+      ~SplitCtx() { h->cq_split_ctx = prev; }
+    } sctx(h);
+    SDC_TRY(blocked_qr(h, S, m, (int)m, n, f));
+  }
   if (rtest_slot >= 0) {
     k_rtest_cols<<<cdiv((long long)n * 32, 256), 256, 0, h->st>>>(S, m, h->Rprev, n, h->vec,
                                                                   h->vec + h->n_max);
@@ -1219,10 +1285,23 @@ int stream_dep(sdc_handle* h, cudaStream_t from, cudaStream_t to, cudaEvent_t ev
   return 0;
 }
 
+// split CholeskyQR2 panels that broke down since the last call (the fallback kernel factored
+// them, correctly but slowly): counted, and mode 1 is switched off for this handle
+void note_split_breakdowns(sdc_handle* h, unsigned nbrk) {
+  if (!nbrk) return;
+  h->sched[SDC_SCHED_CQ_SPLIT_BREAKDOWNS] += nbrk;
+  if (h->cq_split == 1) h->cq_split = 0;
+}
+
 int check_barrier(sdc_handle* h) {
-  unsigned int err = 0;
+  unsigned int err = 0, nbrk = 0;
   SDC_CK(cudaMemcpyAsync(&err, h->bar + 1, sizeof(err), cudaMemcpyDeviceToHost, h->st));
+  if (h->cqs_sync) {
+    SDC_CK(cudaMemcpyAsync(&nbrk, h->cqs_sync + 2, sizeof(nbrk), cudaMemcpyDeviceToHost, h->st));
+    SDC_CK(cudaMemsetAsync(h->cqs_sync + 2, 0, sizeof(unsigned), h->st));
+  }
   SDC_CK(cudaStreamSynchronize(h->st));
+  note_split_breakdowns(h, nbrk);
   if (err) {
     set_err("panel grid barrier timed out (co-residency violated?)");
     return SDC_ERR_CUDA;
@@ -1338,6 +1417,11 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
     SDC_CK(cudaMemcpyAsync(h->hflags + 2, h->alt.bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   else
     h->hflags[2] = 0;
+  h->hflags[3] = 0;
+  if (h->cqs_sync) {
+    SDC_CK(cudaMemcpyAsync(h->hflags + 3, h->cqs_sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+    SDC_CK(cudaMemsetAsync(h->cqs_sync + 2, 0, sizeof(unsigned), h->st));
+  }
   return 0;
 }
 
@@ -1520,6 +1604,12 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (!rc && cudaMemset(h->llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)) != cudaSuccess) rc = SDC_ERR_CUDA;
   ALLOC(h->cqbuf, CQ_DOUBLES);
   if (!rc && cudaMemset(h->cqbuf, 0, CQ_DOUBLES * sizeof(double)) != cudaSuccess) rc = SDC_ERR_CUDA;
+  if (!rc && 2LL * n_max > 4096) {   // split CholeskyQR2 panels (tall stacks only)
+    ALLOC(h->cqs, CQS_DOUBLES);
+    void* q = nullptr;
+    if (!rc && cudaMalloc(&q, 64) != cudaSuccess) rc = SDC_ERR_NOMEM;
+    else if (!rc) { h->allocs.push_back(q); h->cqs_sync = (unsigned*)q; cudaMemset(q, 0, 64); }
+  }
   ALLOC(h->pmA, (n / SEL_T + 1) * n);
   if (h->pencil) ALLOC(h->pmB, (n / SEL_T + 1) * n);
   ALLOC(h->vec, 4 * n + 64);
@@ -1599,6 +1689,11 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
+  if (const char* e = getenv("SDC_UPD_TILE")) h->upd_tile = atoi(e);
+  if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
+  if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
+  if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
+  if (const char* e = getenv("SDC_SPLIT_EFF")) h->split_eff = atof(e);
   if (const char* e = getenv("SDC_GEMM_VARIANT")) h->gemm_force = h->alt.gemm_force = atoi(e);
   if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
@@ -1691,6 +1786,9 @@ int schur_node(sdc_handle* h, cudaStream_t st, int m, double* Tb, long long ldtb
     stats[3] += res.iters;
     // accept only clearly two-sided pairs (same rule as orc_schur_node; reading Q20)
     const bool onesided = res.side < 1e-3 || res.side > 1.0 - 1e-3;
+    if (getenv("SDC_SCHUR_TRACE"))   // decision trace (orc_schur_node's ORC_SCHUR_TRACE format)
+      fprintf(stderr, "node o=%d m=%d att=%d a=%.6f iters=%d status=%d r=%d metric=%.3e side=%.3e\n", o, m, att, a,
+              res.iters, res.status, res.r, res.metric, res.side);
     if (res.status != 0 || onesided) {   // a one-sided pair's split is incidental
       stats[1]++;
       if (res.side > 0.95) hi = a;          // every eigenvalue left of the line
@@ -1705,6 +1803,121 @@ int schur_node(sdc_handle* h, cudaStream_t st, int m, double* Tb, long long ldtb
     return 0;
   }
   stats[2]++;   // 16 failed attempts: an unsplit leaf
+  return 0;
+}
+
+// ---- batched small blocks of the recursion (schur_batched.cuh) ---------------------------
+// Device workspace of one wave: block lists, per-block results and scratch slots.
+struct SchurWave {
+  int cap = 0;
+  int *off = nullptr, *ord = nullptr, *r = nullptr, *stats = nullptr;
+  double *metric = nullptr, *scratch = nullptr;
+  void release() {
+    for (void* p : {(void*)off, (void*)ord, (void*)r, (void*)stats, (void*)metric, (void*)scratch})
+      if (p) cudaFree(p);
+    *this = SchurWave();
+  }
+  int reserve(int nb) {
+    if (nb <= cap) return 0;
+    release();
+    if (cudaMalloc(&off, sizeof(int) * nb) || cudaMalloc(&ord, sizeof(int) * nb) ||
+        cudaMalloc(&r, sizeof(int) * nb) || cudaMalloc(&stats, sizeof(int) * 4 * nb) ||
+        cudaMalloc(&metric, sizeof(double) * nb) ||
+        cudaMalloc(&scratch, sizeof(double) * (size_t)SB_SLOT * nb)) {
+      release();
+      set_err("sdc_schur: out of device memory (batched blocks)");
+      return SDC_ERR_NOMEM;
+    }
+    cap = nb;
+    return 0;
+  }
+};
+constexpr int SCHUR_WAVE_MAX = 148 * 8;   // blocks per launch (scratch: 160 KB per block)
+
+// One launch of k_schur_leaves over the blocks (off[i], ord[i]) of T, all of order <= BAT_NMAX,
+// sorted by the caller so that max_ord bounds them; results to the host vectors.  Q_b of
+// accepted blocks stay in w.scratch (slot 3) for the apply kernels.
+int schur_leaves_launch(sdc_handle* h, cudaStream_t st, SchurWave& w, double* T, long long ldt, int key_off,
+                        int leaf, unsigned long long seed, int max_iters, double tol, const int* off,
+                        const int* ord, int nb, int max_ord, int* r_out, int* stats_out, double* metric_out) {
+  static DevOnce attr;
+  if (!attr.has(h->device)) {
+    SDC_CK(cudaFuncSetAttribute(k_schur_leaves, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)bq_smem_bytes(BAT_NMAX)));
+    SDC_CK(cudaFuncSetAttribute(k_schur_apply_left, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)SB_APPLY_SMEM));
+    SDC_CK(cudaFuncSetAttribute(k_schur_apply_right, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)SB_APPLY_SMEM));
+    attr.set(h->device);
+  }
+  SDC_TRY(w.reserve(nb));
+  SDC_CK(cudaMemcpyAsync(w.off, off, sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  SDC_CK(cudaMemcpyAsync(w.ord, ord, sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+  SchurLeafArgs a{T, ldt, w.off, w.ord, key_off, leaf, seed, max_iters, tol, w.scratch, w.r, w.stats, w.metric,
+                  getenv("SDC_SCHUR_TRACE") ? 1 : 0};
+  k_schur_leaves<<<nb, BQ_THREADS, bq_smem_bytes(max_ord), st>>>(a);
+  SDC_LAUNCHED(h);
+  h->sched[SDC_SCHED_SCHUR_BATCH_LAUNCHES]++;
+  h->sched[SDC_SCHED_SCHUR_BATCH_BLOCKS] += nb;
+  SDC_CK(cudaMemcpyAsync(r_out, w.r, sizeof(int) * nb, cudaMemcpyDeviceToHost, st));
+  SDC_CK(cudaMemcpyAsync(stats_out, w.stats, sizeof(int) * 4 * nb, cudaMemcpyDeviceToHost, st));
+  SDC_CK(cudaMemcpyAsync(metric_out, w.metric, sizeof(double) * nb, cudaMemcpyDeviceToHost, st));
+  return 0;
+}
+
+// All blocks of `small` (order <= BAT_NMAX) and their descendants, one level per wave; leaves
+// are appended to blocks.  T (n x n) and Q (n rows) receive the off-diagonal updates.
+int schur_small_waves(sdc_handle* h, cudaStream_t st, int n, double* T, long long ldt, double* Q, long long ldq,
+                      int key_off, int leaf, unsigned long long seed, int max_iters, double tol,
+                      std::vector<std::pair<int, int>> small, std::vector<std::pair<int, int>>& blocks,
+                      int* stats, double* max_metric) {
+  SchurWave w;
+  struct Guard { SchurWave& w; ~Guard() { w.release(); } } guard{w};
+  std::vector<int> off, ord, r, sst;
+  std::vector<double> met;
+  while (!small.empty()) {
+    std::vector<std::pair<int, int>> work, next;
+    for (auto& b : small) {
+      if (b.second <= leaf || b.second < 2) blocks.push_back(b);   // a leaf by size
+      else work.push_back(b);
+    }
+    // by order (descending): each launch's shared memory is sized by its first block
+    std::stable_sort(work.begin(), work.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+      return ((x.second + 15) & ~15) > ((y.second + 15) & ~15);
+    });
+    for (size_t b0 = 0; b0 < work.size();) {
+      const int cls = (work[b0].second + 15) & ~15;
+      size_t b1 = b0;
+      while (b1 < work.size() && b1 - b0 < (size_t)SCHUR_WAVE_MAX && ((work[b1].second + 15) & ~15) == cls) ++b1;
+      const int nb = (int)(b1 - b0);
+      off.resize(nb); ord.resize(nb); r.resize(nb); sst.resize(4 * (size_t)nb); met.resize(nb);
+      int omin = n;
+      for (int i = 0; i < nb; ++i) {
+        off[i] = work[b0 + i].first;
+        ord[i] = work[b0 + i].second;
+        omin = std::min(omin, off[i] + ord[i]);
+      }
+      SDC_TRY(schur_leaves_launch(h, st, w, T, ldt, key_off, leaf, seed, max_iters, tol, off.data(), ord.data(),
+                                  nb, cls, r.data(), sst.data(), met.data()));
+      SchurApplyArgs ap{T, ldt, Q, ldq, n, w.off, w.ord, w.r, w.scratch};
+      if (n - omin > 0) {
+        k_schur_apply_left<<<dim3(cdiv(n - omin, 64), nb), 256, SB_APPLY_SMEM, st>>>(ap);
+        SDC_LAUNCHED(h);
+      }
+      k_schur_apply_right<<<dim3(2 * cdiv(n, 64), nb), 256, SB_APPLY_SMEM, st>>>(ap);
+      SDC_LAUNCHED(h);
+      SDC_CK(cudaStreamSynchronize(st));
+      for (int i = 0; i < nb; ++i) {
+        for (int q = 0; q < 4; ++q) stats[q] += sst[4 * (size_t)i + q];
+        if (r[i] == 0) { blocks.push_back({off[i], ord[i]}); continue; }
+        *max_metric = std::max(*max_metric, met[i]);
+        next.push_back({off[i], r[i]});
+        next.push_back({off[i] + r[i], ord[i] - r[i]});
+      }
+      b0 = b1;
+    }
+    small.swap(next);
+  }
   return 0;
 }
 }  // namespace
@@ -1750,15 +1963,16 @@ int sdc_schur_keyed(sdc_handle* h, void* stream, int n, const double* A, int lda
     SDC_LAUNCHED(h);
     for (int q = 0; q < 4; ++q) stats[q] = 0;
     *max_metric = 0.0;
-    std::vector<std::pair<int, int>> stack{{0, n}};
-    int nb = 0;
+    std::vector<std::pair<int, int>> stack{{0, n}}, small, blocks;
     while (!stack.empty()) {
       const int o = stack.back().first, m = stack.back().second;
       stack.pop_back();
+      // blocks of order <= 64 wait for the batched waves below (one launch per recursion level)
+      if (h->schur_batch && m <= BAT_NMAX) { small.push_back({o, m}); continue; }
       int r = 0;
       SDC_TRY(schur_node(h, st, m, T + o + (long long)o * ldt, ldt, key_off + o, leaf, seed, max_iters, tol,
                          Qb, m, wk, &r, stats, max_metric));
-      if (r == 0) { blk_off[nb] = o; blk_size[nb] = m; ++nb; continue; }
+      if (r == 0) { blocks.push_back({o, m}); continue; }
       const int nr = n - o - m;
       if (nr > 0) {   // T(o:o+m, o+m:n) = Qb^T T(o:o+m, o+m:n)
         double* Tr = T + o + (long long)(o + m) * ldt;
@@ -1781,7 +1995,11 @@ int sdc_schur_keyed(sdc_handle* h, void* stream, int n, const double* A, int lda
       stack.push_back({o + r, m - r});   // trailing (Re < a), processed second
       stack.push_back({o, r});           // leading (Re > a), processed first
     }
-    *nblk = nb;
+    SDC_TRY(schur_small_waves(h, st, n, T, ldt, Q, ldq, key_off, leaf, seed, max_iters, tol, small, blocks,
+                              stats, max_metric));
+    std::sort(blocks.begin(), blocks.end());   // by offset: the order of the depth-first recursion
+    for (size_t i = 0; i < blocks.size(); ++i) { blk_off[i] = blocks[i].first; blk_size[i] = blocks[i].second; }
+    *nblk = (int)blocks.size();
     SDC_CK(cudaStreamSynchronize(st));
     return 0;
   };
@@ -1814,6 +2032,29 @@ int sdc_schur_node(sdc_handle* h, void* stream, int m, double* Tb, int ldtb, int
   if (!r || !stats || !max_metric) { set_err("NULL host output"); return -13; }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   h->st = st;
+  if (h->schur_batch && m <= BAT_NMAX) {
+    // the same kernel (and so the same decisions) as the batched waves of sdc_schur_keyed
+    *r = 0;
+    if (m <= leaf || m < 2) return 0;
+    SchurWave w;
+    struct Guard { SchurWave& w; ~Guard() { w.release(); } } guard{w};
+    const int off0 = 0;
+    int rr = 0, sst[4] = {0, 0, 0, 0};
+    double met = 0.0;
+    // key_off is the block's own global offset (its local offset in Tb is 0)
+    SDC_TRY(schur_leaves_launch(h, st, w, Tb, ldtb, key_off, leaf, seed, max_iters, tol, &off0, &m, 1,
+                                (m + 15) & ~15, &rr, sst, &met));
+    SDC_CK(cudaStreamSynchronize(st));
+    for (int q = 0; q < 4; ++q) stats[q] += sst[q];
+    if (rr > 0) {
+      *max_metric = std::max(*max_metric, met);
+      SDC_CK(cudaMemcpy2DAsync(Qb, sizeof(double) * ldqb, w.scratch + 3 * BAT_NMAX * BAT_NMAX, sizeof(double) * m,
+                               sizeof(double) * m, m, cudaMemcpyDeviceToDevice, st));
+      SDC_CK(cudaStreamSynchronize(st));
+    }
+    *r = rr;
+    return 0;
+  }
   double *Vb = nullptr, *Gb = nullptr, *Ab = nullptr, *sc = nullptr;
   const size_t mm = (size_t)m * m;
   int rc = 0;
@@ -2150,6 +2391,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   }
   SDC_CK(cudaStreamSynchronize(h->st));
   if (h->hflags[1] || h->hflags[2]) { set_err("panel grid barrier timed out (co-residency violated?)"); return SDC_ERR_CUDA; }
+  note_split_breakdowns(h, h->hflags[3]);
   const double* sc = h->hscal;
   for (int j = 1; j < std::min(hist_cap, p); ++j) hbuf[3 * j + 2] = sc[SCAL_HIST + j];
   if (hist_cap > 0) memcpy(hist, hbuf.data(), sizeof(double) * hbuf.size());

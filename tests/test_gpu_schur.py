@@ -82,3 +82,67 @@ def test_schur_unsplittable(orc, handle):
     A = 2.0 * np.eye(5)
     blocks, info = compare(orc, handle, A, 1, 1)
     assert blocks == [(0, 5)] and info["unsplit"] == 1
+
+
+# ---- batched small blocks (schur_batched.cuh): blocks of order <= 64 run one CTA per block,
+# one launch per recursion level ---------------------------------------------------------
+# Cases whose oracle decisions are stable under relative input noise up to 2e-14
+# (test_oracle_schur.py "batch96" / "batch128" / "batch160"): the batched kernel's contractions
+# run in a different order than the large-n path's, so the 4e-16 margin of the cases above
+# is not enough -- e.g. (128, 1, seed 1) passes it, and the two sides still accept different
+# valid splits of one 8 x 8 block (r = 2 at pass 11 vs r = 4 at pass 9, reading Q20).
+BATCH_CASES = [(96, 1, 6), (128, 1, 13), (160, 2, 32)]
+
+
+@pytest.mark.parametrize("n,leaf,seed", BATCH_CASES)
+def test_schur_batched_blocks_parity(orc, handle, n, leaf, seed):
+    A, V, eig = inputs.normal_random_eigs(n, 15 + n, 16 + n)
+    handle.schedule_counters(reset=True)
+    blocks, info = compare(orc, handle, A, leaf, seed)
+    c = handle.schedule_counters()
+    assert c["schur_batch_launches"] > 0 and c["schur_batch_blocks"] >= len(blocks) // 2
+    assert all(m <= 2 for _, m in blocks)
+
+
+def test_schur_batched_matches_unbatched(orc, monkeypatch):
+    # the large-n kernel sequence on every block (SDC_SCHUR_BATCH=0) takes the same decisions
+    from paper_1011_3077_b200 import api
+    A, V, eig = inputs.normal_random_eigs(128, 15 + 128, 16 + 128)
+    seed = 13
+    res = []
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SDC_SCHUR_BATCH", mode)
+        h = api.Handle(128)
+        Q, T, blocks, info = h.schur(dev(A), leaf=1, seed=seed)
+        c = h.schedule_counters()
+        assert (c["schur_batch_launches"] > 0) == (mode == "1")
+        res.append((blocks, info["splits"], info["failed_attempts"], info["unsplit"], h.launches))
+        h.close()
+    assert res[0][:4] == res[1][:4]
+    assert res[0][4] * 10 <= res[1][4]     # >= 10x fewer kernel launches per decomposition
+
+
+def test_schur_batched_valid_decomposition(handle):
+    # a case whose oracle decisions are NOT margin-stable (block lists may differ between two
+    # valid implementations, reading Q20): check what is unique -- A = Q T Q^T, Q
+    # orthogonal, T block triangular with blocks <= 2, block spectra = eig(A)
+    n = 300
+    A, V, eig = inputs.normal_random_eigs(n, 15 + n, 16 + n)
+    handle.schedule_counters(reset=True)
+    Qg, Tg, blocks, info = handle.schur(dev(A), leaf=1, seed=7)
+    assert handle.schedule_counters()["schur_batch_blocks"] > n // 2
+    Q, T = Qg.cpu().numpy(), Tg.cpu().numpy()
+    assert sum(m for _, m in blocks) == n and all(m <= 2 for _, m in blocks) and info["unsplit"] == 0
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13 * n
+    mask = np.zeros((n, n), bool)
+    for b0, m in blocks:
+        mask[b0:b0 + m, b0:b0 + m] = True
+    assert np.all(T[np.tril(np.ones((n, n), bool), -1) & ~mask] == 0.0)
+    bound = (info["max_metric"] * max(1, info["splits"]) + 1e-13) * np.linalg.norm(A, 1)
+    assert np.linalg.norm(Q @ T @ Q.T - A, 1) <= 2 * bound
+    ev = np.concatenate([np.linalg.eigvals(T[b0:b0 + m, b0:b0 + m]) for b0, m in blocks])
+    ref = np.linalg.eigvals(A)
+    from scipy.optimize import linear_sum_assignment
+    D = np.abs(ev[:, None] - ref[None, :])
+    ri, ci = linear_sum_assignment(D)
+    assert np.max(D[ri, ci]) <= 1e-8
