@@ -133,6 +133,7 @@ struct sdc_handle {
   // its own split-K workspace (Wp2, W2, Zb2)
   bool lookahead = true;
   bool on_side = false;                // issuing on the look-ahead side stream
+  bool in_alt = false;                 // issuing on the second factorization context
   bool two_chains = false;             // both factorization contexts busy (pencil, Alg. 4)
   bool xpass_pending = false;          // la_fork / la_B recorded by the previous IRS pass
   bool xpass_on = false;               // cross-pass look-ahead in the fixed-mode pass loop
@@ -153,8 +154,6 @@ struct sdc_handle {
   unsigned* cqs_sync = nullptr;
   bool schur_batch = true;             // SDC_SCHUR_BATCH: blocks of order <= 64 of the recursion in
                                        // one launch per level (schur_batched.cuh)
-  int upd_tile = 0;                    // SDC_UPD_TILE: 1 = 128x128 reduce-add update tiles (1 CTA/SM)
-  double split_eff = 0.9;              // SDC_SPLIT_EFF: wanted last-wave fill of split-K grids
   cudaStream_t st_hi = nullptr;
   cudaEvent_t la_fork = nullptr, la_fac = nullptr, la_B = nullptr, la_join = nullptr;
   double *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr;
@@ -251,8 +250,8 @@ void swap_ctx(sdc_handle* h) {
 }
 struct AltScope {   // issue on the second context for the scope's lifetime
   sdc_handle* h;
-  explicit AltScope(sdc_handle* h_) : h(h_) { swap_ctx(h); }
-  ~AltScope() { swap_ctx(h); }
+  explicit AltScope(sdc_handle* h_) : h(h_) { swap_ctx(h); h->in_alt = true; }
+  ~AltScope() { swap_ctx(h); h->in_alt = false; }
 };
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -295,7 +294,7 @@ struct ProfScope {
     if (h->prof_on && e0 >= 0) {
       int e1 = prof_event(h);
       if (e1 >= 0) {
-        const int tag = (h->st == h->st_hi ? 1 : 0) | (h->on_side ? 2 : 0);   // stream of the launch
+        const int tag = (h->st == h->st_hi ? 1 : 0) | (h->on_side ? 2 : 0) | (h->in_alt ? 4 : 0);   // stream
         h->recs.push_back({cls, e0, e1, work, tag});
         if (sub >= 0) h->recs.push_back({sub, e0, e1, work, tag});
       }
@@ -354,8 +353,6 @@ using TmaS = TmaTile<64, 64, 32, 32, 6>;        // small grids, 4 consumer warps
 using TmaU = TmaTile<128, 64, 64, 32, 4, 2>;    // rank-nb updates: 2 CTAs/SM, epilogue overlap
 using TmaC = TmaTile<128, 128, 64, 32, 3, 1, true>;  // K <= 256 updates, C tile prefetched by TMA
 using TmaR = TmaTile<128, 64, 64, 32, 3, 2, false, true>;  // updates with beta = 1: bulk reduce-add
-using TmaR2 = TmaTile<128, 128, 64, 32, 4, 1, false, true>;  // same, 128x128 tiles, 1 CTA/SM
-
 template <class T, bool TA, bool TB, int VEC>
 int launch_gemm_t(sdc_handle* h, const GemmArgs& g, int splits) {
   using Sm = GemmSmem<T, TA, TB>;
@@ -506,11 +503,9 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
     // would hold every SM until the whole update finished, and the critical chain's kernels
     // (panels, next-block updates, reductions) on the high-priority stream would queue
     // behind it; one-tile CTAs retire continuously, so the scheduler can hand SMs to them.
-    const bool big = h->upd_tile == 1 && M >= 1024 && N >= 1024;
     if (v == 3 && (h->on_side || h->two_chains) && !h->side_persist) {
       if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
-        return big ? launch_tma_t<TmaR2>(h, A, lda, B, ldb, g, splits)
-                   : launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
+        return launch_tma_t<TmaR>(h, A, lda, B, ldb, g, splits);
       return launch_tma_t<TmaU>(h, A, lda, B, ldb, g, splits);
     }
     if (pm == 2 || (pm == 1 && v == 3)) {
@@ -520,8 +515,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
         case 2: return launch_tma_persist<TmaS>(h, A, lda, B, ldb, g, splits);
         case 3:
           if (h->red_mode && beta == 1.0 && D2 == nullptr && g.red_ok)
-            return big ? launch_tma_persist<TmaR2>(h, A, lda, B, ldb, g, splits)
-                       : launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
+            return launch_tma_persist<TmaR>(h, A, lda, B, ldb, g, splits);
           return launch_tma_persist<TmaU>(h, A, lda, B, ldb, g, splits);
         default: break;
       }
@@ -562,7 +556,7 @@ int pick_splits(sdc_handle* h, int tiles, int K, long long cap) {
     const long long ctas = (long long)tiles * s;
     const long long waves = (ctas + P - 1) / P;
     const double eff = (double)ctas / (double)(waves * P);
-    if (ctas >= 2LL * P && eff >= h->split_eff) return s;
+    if (ctas >= 2LL * P && eff >= 0.9) return s;
     if (eff > best_eff + 1e-9 || (ctas < 2LL * P && s == smax)) { best_eff = eff; best = s; }
   }
   return best;
@@ -1689,11 +1683,9 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
-  if (const char* e = getenv("SDC_UPD_TILE")) h->upd_tile = atoi(e);
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
-  if (const char* e = getenv("SDC_SPLIT_EFF")) h->split_eff = atof(e);
   if (const char* e = getenv("SDC_GEMM_VARIANT")) h->gemm_force = h->alt.gemm_force = atoi(e);
   if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;

@@ -18,6 +18,7 @@ def main():
               ("TN rank-128 update", True, False, 2 * n, n, 128),
               ("TN rank-256 update", True, False, 2 * n, n, 256),
               ("TN rank-256 update b=0", True, False, 2 * n, n, -256),
+              ("TN rank-512 update", True, False, 2 * n, n, 512),
               ("TN W0 (no split-K)", True, False, 64, n, 2 * n)]
     for name, ta, tb, M, N, K in shapes:
         beta = 1.0
