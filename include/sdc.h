@@ -103,7 +103,8 @@ typedef struct sdc_handle sdc_handle;
  * + ~ n_max^2/32 (selection partials) + ~ 20 M doubles (split-K partials of both streams)
  * for RNEP; pencil handles add 9 n_max^2 (left stack, A'_j/B'_j x2, Bhat, Q_L, V_L^T).
  * The second factorization context (allocated on the first monitor-mode or pencil call)
- * adds 9 n_max^2 (Y, Y^T, complement, G1-G3) + ~ 10 M doubles.  At n_max = 16384: 41 GB
+ * adds 9 n_max^2 (Y, Y^T, complement, G1-G3) + ~ 10 M doubles; handles with 2 n_max > 4096
+ * add 0.8 M doubles for the split CholeskyQR2 panel chain.  At n_max = 16384: 41 GB
  * (RNEP), 60 GB with the second context.  The caller's current device is restored on
  * return (as by every entry point below).  Supported: 2 <= n_max <= 24576.  Returns 0 or <0. */
 int sdc_create(sdc_handle** h, int device, int n_max, int pencil);
@@ -198,13 +199,18 @@ int sdc_split_batched(sdc_handle* h, void* stream, int batch, int n, const doubl
  * interval to the line.  On acceptance E21 := 0,
  * T and Q are updated by the block's Q_b and the two diagonal blocks are processed depth
  * first (eigenvalues right of the line first).  16 failed attempts: an unsplit leaf.
+ * Blocks of order <= 64 are deferred and run BATCHED: one launch per recursion level, one CTA
+ * per block running the whole node in shared memory (same decisions and draws; csrc/
+ * schur_batched.cuh, SDC_SCHUR_BATCH=0 disables it), then two launches applying the accepted
+ * Q_b to T's strips and to Q.  The draws are keyed by the block, so the order of processing
+ * does not change them; the block list is returned sorted by offset (= depth-first order).
  *  1 h, 2 stream, 3 n (<= n_max), 4 A, 5 lda (device input)
  *  6 leaf        >= 1: largest diagonal block left unsplit (1: real Schur-like form)
  *  7 seed        generator seed (lines and Haar matrices)
  *  8 max_iters, 9 tol   per split (monitor mode)
  * 10 Q, 11 ldq  out (device): orthogonal n x n
  * 12 T, 13 ldt  out (device): block upper triangular, exactly 0 below the diagonal blocks
- * 14 blk_off, 15 blk_size   HOST out (n ints each): the diagonal blocks, processing order
+ * 14 blk_off, 15 blk_size   HOST out (n ints each): the diagonal blocks by increasing offset
  * 16 nblk       HOST out: number of blocks
  * 17 stats      HOST out (4 ints): accepted splits, failed attempts, unsplit leaves, passes
  * 18 max_metric HOST out: largest accepted ||E21||_1/||A_block||_1 (the backward error per split)
@@ -230,7 +236,9 @@ int sdc_schur_keyed(sdc_handle* h, void* stream, int n, const double* A, int lda
  *        (m <= leaf, or a 2x2 with complex eigenvalues) or an unsplit block (Tb unchanged)
  *  14 stats, 15 max_metric  HOST, ACCUMULATED (not reset) as in sdc_schur
  * Errors: -3 m, -4 Tb, -5 ldtb, -6 key_off, -7 leaf, -9 max_iters, -10 tol, -11 Qb, -12 ldqb,
- * -13 NULL host output.  Allocates 3 m x m scratch matrices; synchronises `stream`. */
+ * -13 NULL host output.  Allocates 3 m x m scratch matrices; synchronises `stream`.  Blocks of
+ * order <= 64 run in the batched kernel of sdc_schur (one block), so a node solved on its own
+ * takes the decisions the whole recursion takes there. */
 int sdc_schur_node(sdc_handle* h, void* stream, int m, double* Tb, int ldtb, int key_off, int leaf,
                    unsigned long long seed, int max_iters, double tol, double* Qb, int ldqb, int* r,
                    int* stats, double* max_metric);

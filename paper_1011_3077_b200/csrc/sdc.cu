@@ -142,6 +142,8 @@ struct sdc_handle {
   // GEMM schedule knobs (env at sdc_create; DESIGN.md §6 table): persistent grids for short-K
   // updates (0 off, 1 short-K, 2 every TMA GEMM), bulk reduce-add epilogue for beta = 1,
   // persistent grids on the side stream / second chain too
+  int l2_hints = 0;                    // SDC_L2_HINTS (persistent update kernel): 1 reduce-add evict_first,
+                                       // 2 operand loads evict_last
   int persist_mode = 1, red_mode = 1;
   bool side_persist = false;
   // CholeskyQR2 panel as a chain of small kernels (cqr_split.cuh): SDC_CQ_SPLIT 0 never, 1 tall
@@ -167,8 +169,9 @@ struct sdc_handle {
     double *Y = nullptr, *Yt = nullptr, *Tb = nullptr, *Tob = nullptr, *Tobt = nullptr, *Zb = nullptr,
            *Gb = nullptr, *tau = nullptr, *Wp = nullptr, *W = nullptr, *gbuf = nullptr, *llbuf = nullptr,
            *vec = nullptr, *Wp2 = nullptr, *W2 = nullptr, *Zb2 = nullptr, *C = nullptr, *G1 = nullptr,
-           *G2 = nullptr, *G3 = nullptr, *cqbuf = nullptr;
+           *G2 = nullptr, *G3 = nullptr, *cqbuf = nullptr, *cqs = nullptr;
     unsigned int* bar = nullptr;
+    unsigned int* cqs_sync = nullptr;
     unsigned long long bar_count = 0;
     unsigned ll_epoch = 0;
     int gemm_force = -1;
@@ -246,6 +249,7 @@ void swap_ctx(sdc_handle* h) {
   std::swap(h->C, a.C); std::swap(h->G1, a.G1); std::swap(h->G2, a.G2); std::swap(h->G3, a.G3);
   std::swap(h->gemm_force, a.gemm_force);
   std::swap(h->cqbuf, a.cqbuf);
+  std::swap(h->cqs, a.cqs); std::swap(h->cqs_sync, a.cqs_sync);
   std::swap(h->xpass_pending, a.xpass_pending);
 }
 struct AltScope {   // issue on the second context for the scope's lifetime
@@ -487,7 +491,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (tma) {
     h->sched[SDC_SCHED_GEMM_TMA]++;
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
-                  (int)(al16(C, ldc) && M % 2 == 0), kupper};
+                  (int)(al16(C, ldc) && M % 2 == 0), h->l2_hints, kupper};
     int v = h->gemm_force;
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
@@ -666,7 +670,7 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
   if (nb == NB && h->cqs && m <= CQS_GMAX * CQS_ROWS &&
       (h->cq_split == 2 ? m >= 128
-                        : (h->cq_split == 1 && h->cq_split_ctx && m > h->cq_split_rows && !h->share_sms)))
+                        : (h->cq_split == 1 && h->cq_split_ctx && m > h->cq_split_rows)))
     return panel_split(h, P, ldp, m, Y, ldy, Yt, ldyt, T, tau, zero_above);
   // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange); taller panels: several
   // 16-CTA clusters with a two-level exchange (DSMEM inside, L2 between cluster leaders);
@@ -1228,6 +1232,7 @@ int ensure_alt(sdc_handle* h) {
   ALLOC(a.gbuf, 2 * ((size_t)h->num_sms + 1) * PANEL_NB);
   ALLOC(a.llbuf, PANEL_LL_DOUBLES);
   ALLOC(a.cqbuf, CQ_DOUBLES);
+  if (h->cqs) ALLOC(a.cqs, CQS_DOUBLES);
   ALLOC(a.vec, 4 * n + 64);
   ALLOC(a.C, 2 * nn);
   ALLOC(a.G1, nn); ALLOC(a.G2, nn); ALLOC(a.G3, nn);
@@ -1255,6 +1260,12 @@ int ensure_alt(sdc_handle* h) {
   h->allocs.push_back(q);
   a.bar = (unsigned*)q;
   SDC_CK(cudaMemset(a.bar, 0, 64));
+  if (a.cqs) {
+    SDC_CK(cudaMalloc(&q, 64));
+    h->allocs.push_back(q);
+    a.cqs_sync = (unsigned*)q;
+    SDC_CK(cudaMemset(q, 0, 64));
+  }
   SDC_CK(cudaMemset(a.llbuf, 0, PANEL_LL_DOUBLES * sizeof(double)));
   SDC_CK(cudaMemset(a.cqbuf, 0, CQ_DOUBLES * sizeof(double)));
   SDC_CK(cudaStreamCreateWithFlags(&a.st, cudaStreamNonBlocking));
@@ -1411,10 +1422,14 @@ int enqueue_finish(sdc_handle* h, int n, const double* A, long long lda, const d
     SDC_CK(cudaMemcpyAsync(h->hflags + 2, h->alt.bar + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
   else
     h->hflags[2] = 0;
-  h->hflags[3] = 0;
+  h->hflags[3] = h->hflags[4] = 0;
   if (h->cqs_sync) {
     SDC_CK(cudaMemcpyAsync(h->hflags + 3, h->cqs_sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
     SDC_CK(cudaMemsetAsync(h->cqs_sync + 2, 0, sizeof(unsigned), h->st));
+  }
+  if (h->alt.cqs_sync) {   // (the second context's chains were joined into this stream before)
+    SDC_CK(cudaMemcpyAsync(h->hflags + 4, h->alt.cqs_sync + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, h->st));
+    SDC_CK(cudaMemsetAsync(h->alt.cqs_sync + 2, 0, sizeof(unsigned), h->st));
   }
   return 0;
 }
@@ -1683,6 +1698,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
+  if (const char* e = getenv("SDC_L2_HINTS")) h->l2_hints = atoi(e);
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
@@ -2383,7 +2399,7 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
   }
   SDC_CK(cudaStreamSynchronize(h->st));
   if (h->hflags[1] || h->hflags[2]) { set_err("panel grid barrier timed out (co-residency violated?)"); return SDC_ERR_CUDA; }
-  note_split_breakdowns(h, h->hflags[3]);
+  note_split_breakdowns(h, h->hflags[3] + h->hflags[4]);
   const double* sc = h->hscal;
   for (int j = 1; j < std::min(hist_cap, p); ++j) hbuf[3 * j + 2] = sc[SCAL_HIST + j];
   if (hist_cap > 0) memcpy(hist, hbuf.data(), sizeof(double) * hbuf.size());

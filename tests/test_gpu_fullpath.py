@@ -210,3 +210,32 @@ def test_two_chain_multicluster_stress(sdc):
         assert torch.equal(Q, outs[0][0]) and torch.equal(QL, outs[0][1])
         assert (r, met) == outs[0][2:]
     print("schedule counters:", c)
+
+
+# ---- the split CholeskyQR2 panel chain (csrc/cqr_split.cuh) on the twins: at full size it is
+# the default for every IRS stack panel above 8192 rows (configs[2]-[4] and the pencil's two
+# chains); SDC_CQ_SPLIT_ROWS lowers the threshold so the oracle-sized twins take it ----------
+def test_cfg5_twin_n2304_split_panels(sdc):
+    ref = oracle_cache.case("cfg5_n2304")
+    h = handle_env(sdc, 2304, SDC_CQ_SPLIT_ROWS=128)
+    Q, QL, _, info = run(h, ref.p)
+    c = h.schedule_counters()
+    # every stack panel but the last (m - i0 = 128 + 64 rows) of each of the 30 passes
+    assert c["panel_cq_split"] >= 30 * (2304 // 64 - 2) and c["cq_split_breakdowns"] == 0, c
+    assert c["lookahead_forks"] > 0 and c["panel_cqr_fallback"] == 0, c
+    assert_twin(ref, Q, None, info, 2304)
+    assert info.k == 1152
+
+
+def test_cfg4_twin_n1024_split_panels_two_chains(sdc):
+    # both chains of Alg. 4 run their stack panels as split chains on their own workspaces
+    ref = oracle_cache.case("cfg4_n1024")
+    h = handle_env(sdc, 2049, pencil=True, SDC_CQ_SPLIT_ROWS=128)
+    Q, QL, _, info = run(h, ref.p)
+    c = h.schedule_counters()
+    assert c["ctx_forks"] > 0 and c["panel_cq_split"] >= 2 * 30 * (1024 // 64 - 2), c
+    assert c["cq_split_breakdowns"] == 0, c
+    assert_twin(ref, Q, QL, info, 1024)
+    # bit-identical on a second run (fixed summation orders, no atomics on data)
+    Q2, QL2, _, info2 = run(h, ref.p)
+    assert torch.equal(Q, Q2) and torch.equal(QL, QL2) and info.metric == info2.metric

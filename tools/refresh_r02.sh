@@ -14,5 +14,6 @@ for c in 1 2; do timeout 400 python bench.py --config $c --steps 5 --warmup 3 > 
 timeout 600 python bench.py --config 3 --steps 3 --warmup 3 > $OUT/bench_c3.json 2> $OUT/bench_c3.err
 for c in 4 6 9; do timeout 900 python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err; done
 for c in 7 8 10; do timeout 600 python bench.py --config $c --steps 3 --warmup 3 > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err; done
+timeout 600 python bench.py --config 8 --leaf 1 --steps 2 --warmup 1 > $OUT/bench_c8_leaf1.json 2> $OUT/bench_c8_leaf1.err
 timeout 900 python bench.py --impl reference --steps 1 --warmup 0 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 tail -n 3 $OUT/gpu_tests.log; cat $OUT/bench_default.json
