@@ -35,7 +35,6 @@ struct TmaGemmArgs {
   int kchunk;             // K per z-slice (multiple of 16)
   long long c_zstride;    // element stride between z-slices of C
   int red_ok;             // RED tiles: C += alpha A^T B may use bulk reduce-add (host-checked)
-  int l2_hints;           // bit 0: reduce-add traffic evict_first, bit 1: operand loads evict_last
   int kupper;             // B_s upper triangular (B_s(k, n) = 0 for k > n): a tile's K loop
                           // stops at its last column (skips products with zeros only)
 };
@@ -84,23 +83,6 @@ SDC_DEV void mbar_wait(uint64_t* bar, unsigned parity) {
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   } while (!ok);
-}
-SDC_DEV uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-SDC_DEV uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-SDC_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
 }
 SDC_DEV void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -371,7 +353,6 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
   }
   __syncthreads();
 
-  const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
   // producer cursor (thread 0): the (tile, k-slice) stream of this CTA
   const bool producer = (threadIdx.x == 0);
   int p_tile = blockIdx.x, p_kt = 0, p_nk = 0, p_m0 = 0, p_n0 = 0, p_kb = 0;
@@ -399,13 +380,8 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
     unsigned char* st = base + (size_t)s * T::STAGE_BYTES;
     mbar_expect_tx(full + s, T::STAGE_BYTES);
     const int k = p_kb + p_kt * T::BK;
-    if (g.l2_hints & 2) {
-      tma_load_2d_hint(st, &tmA, k, p_m0, full + s, pol_last);
-      tma_load_2d_hint(st + T::A_BYTES, &tmB, k, p_n0, full + s, pol_last);
-    } else {
-      tma_load_2d(st, &tmA, k, p_m0, full + s);
-      tma_load_2d(st + T::A_BYTES, &tmB, k, p_n0, full + s);
-    }
+    tma_load_2d(st, &tmA, k, p_m0, full + s);
+    tma_load_2d(st + T::A_BYTES, &tmB, k, p_n0, full + s);
     ++g_issue;
     ++p_kt;
   };
@@ -485,17 +461,10 @@ gemm_tn_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA,
           __syncwarp();
           const int n = n0 + wn * T::WN + j * 8 + lane;
           if (lane < 8 && rows > 0 && n < g.N) {
-            if (g.l2_hints & 1)
-              asm volatile(
-                  "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;\n" ::"l"(
-                      C + mw + (long long)n * g.ldc),
-                  "r"(smem_u32(buf + lane * T::RED_LD)), "r"(rows * 8), "l"(pol_first)
-                  : "memory");
-            else
-              asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(
-                               C + mw + (long long)n * g.ldc),
-                           "r"(smem_u32(buf + lane * T::RED_LD)), "r"(rows * 8)
-                           : "memory");
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(
+                             C + mw + (long long)n * g.ldc),
+                         "r"(smem_u32(buf + lane * T::RED_LD)), "r"(rows * 8)
+                         : "memory");
           }
           if (lane < 8) asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }

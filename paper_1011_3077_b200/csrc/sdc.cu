@@ -142,8 +142,6 @@ struct sdc_handle {
   // GEMM schedule knobs (env at sdc_create; DESIGN.md §6 table): persistent grids for short-K
   // updates (0 off, 1 short-K, 2 every TMA GEMM), bulk reduce-add epilogue for beta = 1,
   // persistent grids on the side stream / second chain too
-  int l2_hints = 0;                    // SDC_L2_HINTS (persistent update kernel): 1 reduce-add evict_first,
-                                       // 2 operand loads evict_last
   int persist_mode = 1, red_mode = 1;
   bool side_persist = false;
   // CholeskyQR2 panel as a chain of small kernels (cqr_split.cuh): SDC_CQ_SPLIT 0 never, 1 tall
@@ -491,7 +489,7 @@ int gemm_tn(sdc_handle* h, int M, int N, int K, double alpha, const double* A, l
   if (tma) {
     h->sched[SDC_SCHED_GEMM_TMA]++;
     TmaGemmArgs g{M, N, K, C, ldc, alpha, beta, D2, ldd2, alpha2, kchunk, c_zstride,
-                  (int)(al16(C, ldc) && M % 2 == 0), h->l2_hints, kupper};
+                  (int)(al16(C, ldc) && M % 2 == 0), kupper};
     int v = h->gemm_force;
     const bool cok = beta != 0.0 && splits == 1 && al16(C, ldc) && D2 == nullptr;
     if (v < 0) {
@@ -1698,7 +1696,6 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
-  if (const char* e = getenv("SDC_L2_HINTS")) h->l2_hints = atoi(e);
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
