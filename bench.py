@@ -739,7 +739,10 @@ def main():
     achieved = g_flops / (g_ms / 1e3) / 1e12 if g_ms > 0 else None
     traffic = None
     try:   # DRAM bytes per launch of the representative GEMM launches, from the committed ncu capture
-        tj = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))
+        tpath = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        tj = json.load(open(tpath))
         traffic = {k["shape"]: {"dram_bytes": k["dram_read_bytes"] + k["dram_write_bytes"],
                                 "algorithmic_bytes": k["algorithmic_bytes"]} for k in tj["kernels"]}
         traffic["source"] = tj["source"]
@@ -748,11 +751,12 @@ def main():
     roof = {"bound": "tensor", "kernel": "gemm_tn_tma_kernel / gemm_tn_tma_persist_kernel (all DMMA GEMM launches)",
             "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": traffic,
-            "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r01_fp64_peak_microbench.txt)",
+            "peak_source": "measured DMMA.8x8x4 microbenchmark (profiles/r02_fp64_peak_microbench.txt)",
             "share_of_step": (g_ms / prof_steps) / ms if ms > 0 else None,
             "launches_per_step": g_n // prof_steps, "timed_live": live_prof,
             "flops_per_launch": g_flops / max(1, g_n)}
-    panel = {"bound": "hbm", "kernel": "panel_qr_kernel", "achieved":
+    panel = {"bound": "hbm", "kernel": "panel factorisations: k_cqs_* chains (tall stack panels) + panel_qr_kernel",
+             "achieved":
              (p_bytes / (p_ms / 1e3) / 1e9) if p_ms > 0 else None, "peak": hbm, "unit": "GB/s",
              "peak_source": hbm_src, "share_of_step": (p_ms / prof_steps) / ms if ms > 0 else None,
              "launches_per_step": p_n // prof_steps}

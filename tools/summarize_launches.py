@@ -19,6 +19,8 @@ def kernel_class(name: str) -> str:
         return "gemm_dmma_kernel (DMMA, cp.async)"
     if "panel_qr" in name:
         return "panel_qr_kernel"
+    if "k_cqs_" in name:
+        return "k_cqs_* (split CholeskyQR2 panel chain: 6 kernels per panel)"
     if "sdc::" in name or name.startswith("k_") or "k_split_batched" in name or "trevc" in name:
         return name.split("(")[0].replace("void ", "")
     return "torch (input prep, outside the timed region)"
