@@ -142,6 +142,7 @@ struct sdc_handle {
   // GEMM schedule knobs (env at sdc_create; DESIGN.md §6 table): persistent grids for short-K
   // updates (0 off, 1 short-K, 2 every TMA GEMM), bulk reduce-add epilogue for beta = 1,
   // persistent grids on the side stream / second chain too
+  int split_kmin = 256;                // SDC_SPLIT_KMIN: shortest K slice of a split-K GEMM
   int persist_mode = 1, red_mode = 1;
   bool side_persist = false;
   // CholeskyQR2 panel as a chain of small kernels (cqr_split.cuh): SDC_CQ_SPLIT 0 never, 1 tall
@@ -550,7 +551,7 @@ int gemm_general(sdc_handle* h, bool ta, bool tb, int M, int N, int K, double al
 // split-K factor for a tall-K GEMM with `tiles` output tiles: at least ~2 waves of CTAs,
 // K slices >= 256, and the fewest splits whose last wave is >= 90% full (wave quantisation)
 int pick_splits(sdc_handle* h, int tiles, int K, long long cap) {
-  const int smax = (int)std::max(1LL, std::min<long long>(std::min(K / 256, 64), cap));
+  const int smax = (int)std::max(1LL, std::min<long long>(std::min(K / h->split_kmin, 64), cap));
   const int P = h->num_sms;
   int best = 1;
   double best_eff = 0.0;
@@ -585,7 +586,7 @@ int wy_apply(sdc_handle* h, int trans, int m, int ncols, const double* Y, long l
              const double* Yt, long long ldyt, const double* T, int nb, double* C, long long ldc) {
   if (m <= 0 || ncols <= 0) return 0;
   const int tilesN = cdiv(ncols, 128);
-  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesN), std::max(1, m / 256)));
+  int splits = std::max(1, std::min(cdiv(2 * h->num_sms, tilesN), std::max(1, m / h->split_kmin)));
   int kchunk = cdiv(cdiv(m, splits), 16) * 16;
   splits = cdiv(m, kchunk);
   if ((size_t)splits * nb * ncols > h->wp_elems) {
@@ -785,7 +786,7 @@ int build_tout(sdc_handle* h, int m, int I0, int nbo, const Fac& f) {
   const int rows = m - I0;
   // G = Y_O^T Y_O (split-K TN GEMM + fixed-order sum)
   int splits = std::max(1, std::min(cdiv(2 * h->num_sms, cdiv(nbo, 128) * cdiv(nbo, 128)),
-                                    std::max(1, rows / 256)));
+                                    std::max(1, rows / h->split_kmin)));
   int kchunk = cdiv(cdiv(rows, splits), 16) * 16;
   splits = cdiv(rows, kchunk);
   if ((size_t)splits * nbo * nbo > h->wp_elems) { set_err("build_tout: workspace"); return SDC_ERR_CUDA; }
@@ -1696,6 +1697,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_PERSIST")) h->persist_mode = atoi(e);
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
+  if (const char* e = getenv("SDC_SPLIT_KMIN")) h->split_kmin = std::max(16, atoi(e));
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));

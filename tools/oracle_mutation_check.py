@@ -38,14 +38,40 @@ MUTANTS = [
     ("metric_fro without sqrt", "return sqrt(sa) / fA + (Bh ? sqrt(sb) / fB : 0.0);",
      "return sa / fA + (Bh ? sqrt(sb) / fB : 0.0);"),
     ("accept threshold 1e-3", "#define ORC_SPLIT_ACCEPT 1e-8", "#define ORC_SPLIT_ACCEPT 1e-3", HDR),
+    # widened rows (f1-f4): half-plane map, disk radius, SVD embedding, the recursion's rules, TREVC
+    ("half-plane shifts swapped", "EL(Aj, i, j, n) = EL(A, i, j, lda) - (i == j ? param - 1.0 : 0.0);",
+     "EL(Aj, i, j, n) = EL(A, i, j, lda) - (i == j ? param + 1.0 : 0.0);"),
+    ("disk radius on A side", "EL(Bj, i, j, n) = rho * (pencil ? EL(B, i, j, ldb) : (i == j ? 1.0 : 0.0));",
+     "EL(Bj, i, j, n) = (1.0 / rho) * (pencil ? EL(B, i, j, ldb) : (i == j ? 1.0 : 0.0));"),
+    ("SVD embedding lower block not transposed", "EL(H, m + j, i, N) = EL(A, i, j, lda);",
+     "EL(H, m + (i < n ? i : j), (j < m ? j : i), N) = EL(A, i, j, lda);"),
+    ("recursion: interval end moved the wrong way", "if (res.side > 0.95) hi = a;", "if (res.side > 0.95) lo = a;"),
+    ("recursion: accepts one-sided pairs", "const int onesided = res.side < 1e-3 || res.side > 1.0 - 1e-3;",
+     "const int onesided = 0;"),
+    ("recursion: E21 not zeroed", "EL(Tb, i, j, ldtb) = (i >= r && j < r) ? 0.0 : EL(Ab, i, j, m);",
+     "EL(Tb, i, j, ldtb) = EL(Ab, i, j, m);"),
+    ("plateau rule fires at any level", "met <= 10.0 * tol && met > 0.5 * prev", "met > 0.5 * prev"),
+    ("TREVC numerator drops T_ij X_jj", "double num = EL(T, i, j, ldt) * EL(Xt, j, j, ldx);", "double num = 0.0;"),
+    ("TREVC denominator sign", "double den = EL(T, i, i, ldt) - d;", "double den = d - EL(T, i, i, ldt);"),
 ]
+
+
+CORE = ["tests/test_oracle_factorizations.py", "tests/test_oracle_irs_grurv.py", "tests/test_oracle_step.py"]
+# the widened rows' mutants are judged by the pins of their own rows
+WIDENED = {"half-plane": ["tests/test_oracle_regions.py"], "disk radius": ["tests/test_oracle_regions.py"],
+           "SVD": ["tests/test_oracle_svd.py"], "recursion": ["tests/test_oracle_schur.py"],
+           "plateau": ["tests/test_oracle_schur.py", "tests/test_oracle_regions.py"],
+           "TREVC": ["tests/test_oracle_trevc.py"]}
 
 
 def main():
     origs = {p: open(p).read() for p in (SRC, HDR)}
     failures = []
     try:
+        only = sys.argv[1:]
         for name, old, new, *where in MUTANTS:
+            if only and not any(name.startswith(o) for o in only):
+                continue
             path = where[0] if where else SRC
             for p, text in origs.items():
                 open(p, "w").write(text)
@@ -56,8 +82,8 @@ def main():
                                cwd=ROOT, capture_output=True)
             if r.returncode:
                 print(f"{name}: build failed"); failures.append(name); continue
-            t = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "tests/test_oracle_factorizations.py",
-                                "tests/test_oracle_irs_grurv.py", "tests/test_oracle_step.py"],
+            files = next((v for k, v in WIDENED.items() if name.startswith(k)), CORE)
+            t = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "not gpu"] + files,
                                cwd=ROOT, capture_output=True, text=True)
             caught = t.returncode != 0
             print(f"{'CAUGHT ' if caught else 'MISSED '} {name}")
