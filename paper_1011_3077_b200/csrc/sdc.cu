@@ -142,8 +142,9 @@ struct sdc_handle {
   // GEMM schedule knobs (env at sdc_create; DESIGN.md §6 table): persistent grids for short-K
   // updates (0 off, 1 short-K, 2 every TMA GEMM), bulk reduce-add epilogue for beta = 1,
   // persistent grids on the side stream / second chain too
-  int split_kmin = 256;                // SDC_SPLIT_KMIN: shortest K slice of a split-K GEMM
-  bool la64 = false;                   // SDC_LA64: look-ahead QR also with single-level 64-wide blocks
+  int split_kmin = 128;                // SDC_SPLIT_KMIN: shortest K slice of a split-K GEMM (256 -> 128:
+                                       // config 2 82.8 -> 76.5 ms; the small W0 = Y^T C products of the
+                                       // panel chain were 64 CTAs of 16 K-tiles)
   int persist_mode = 1, red_mode = 1;
   bool side_persist = false;
   // CholeskyQR2 panel as a chain of small kernels (cqr_split.cuh): SDC_CQ_SPLIT 0 never, 1 tall
@@ -852,7 +853,7 @@ inline void choose_nbo(sdc_handle* h, int n, bool two_chains = false) {
 }
 
 inline bool lookahead_qr(const sdc_handle* h, int n) {
-  return h->lookahead && h->st_hi && (h->nbo > NB || h->la64) && n > 2 * h->nbo;
+  return h->lookahead && h->st_hi && h->nbo > NB && n > 2 * h->nbo;
 }
 
 // panels + inner WY updates + T_O of the outer block at I0 (columns I0..I0+nbo-1 only)
@@ -1699,7 +1700,6 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_RED")) h->red_mode = atoi(e);
   if (const char* e = getenv("SDC_SIDE_PERSIST")) h->side_persist = atoi(e) != 0;
   if (const char* e = getenv("SDC_SPLIT_KMIN")) h->split_kmin = std::max(16, atoi(e));
-  if (const char* e = getenv("SDC_LA64")) h->la64 = atoi(e) != 0;
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
