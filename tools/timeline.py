@@ -53,6 +53,7 @@ def run(cfg, n):
     h.profile_read(0)
     h.profile(False)
     print(f"cfg{cfg} n={p.n}: {e0.elapsed_time(e1):.1f} ms (profiled), iters={out[3].iters} k={out[3].k}")
+    print({k: v for k, v in h.schedule_counters().items() if v})
 
 
 if __name__ == "__main__":
