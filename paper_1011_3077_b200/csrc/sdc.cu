@@ -152,6 +152,10 @@ struct sdc_handle {
   // panel of >= 128 rows (tests).  cq_split_ctx: inside such a QR.  A reported breakdown turns
   // mode 1 off for the handle (the fallback is correct but slow).
   int cq_split = 1, cq_split_rows = 8192;
+  // two chains sharing the SMs (monitor mode, pencils): every multi-cluster stack panel takes the
+  // chain -- a cluster launch has to gather 16 SMs of one GPC between the other chain's CTAs,
+  // ordinary CTAs do not (config 3: 2286 -> 2111 ms; alone the cluster kernel is faster there)
+  int cq_split_rows_shared = 4096;
   bool cq_split_ctx = false;
   double* cqs = nullptr;
   unsigned* cqs_sync = nullptr;
@@ -671,7 +675,8 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
           double* Yt, long long ldyt, double* T, double* tau, int zero_above) {
   if (nb == NB && h->cqs && m <= CQS_GMAX * CQS_ROWS &&
       (h->cq_split == 2 ? m >= 128
-                        : (h->cq_split == 1 && h->cq_split_ctx && m > h->cq_split_rows)))
+                        : (h->cq_split == 1 && h->cq_split_ctx &&
+                           m > (h->share_sms ? std::min(h->cq_split_rows, h->cq_split_rows_shared) : h->cq_split_rows))))
     return panel_split(h, P, ldp, m, Y, ldy, Yt, ldyt, T, tau, zero_above);
   // one cluster of <= 16 CTAs when the panel fits (DSMEM exchange); taller panels: several
   // 16-CTA clusters with a two-level exchange (DSMEM inside, L2 between cluster leaders);
@@ -1703,6 +1708,7 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
   if (const char* e = getenv("SDC_SCHUR_BATCH")) h->schur_batch = atoi(e) != 0;
   if (const char* e = getenv("SDC_CQ_SPLIT")) h->cq_split = std::max(0, std::min(2, atoi(e)));
   if (const char* e = getenv("SDC_CQ_SPLIT_ROWS")) h->cq_split_rows = std::max(128, atoi(e));
+  if (const char* e = getenv("SDC_CQ_SPLIT_ROWS_SHARED")) h->cq_split_rows_shared = std::max(128, atoi(e));
   if (const char* e = getenv("SDC_GEMM_VARIANT")) h->gemm_force = h->alt.gemm_force = atoi(e);
   if (const char* e = getenv("SDC_XPASS")) h->xpass_on = atoi(e) != 0;
   if (const char* e = getenv("SDC_PIPELINE")) h->pipeline = atoi(e) != 0;
@@ -2307,8 +2313,11 @@ int sdc_split_region(sdc_handle* h, void* stream, int n, const double* A, int ld
     const long long ld = wld(n);
     struct Share {   // GRURV(j) panels on the second context run next to pass j+1's panels
       sdc_handle* h;
-      explicit Share(sdc_handle* h_) : h(h_) { h->share_sms = true; }
-      ~Share() { h->share_sms = false; }
+      explicit Share(sdc_handle* h_) : h(h_) {
+        h->share_sms = true;
+        h->two_chains = true;   // one-tile update CTAs in both chains, as for the pencil's (config 3: -1%)
+      }
+      ~Share() { h->share_sms = false; h->two_chains = false; }
     } share(h);
     SDC_TRY(enqueue_init(h, n, A, lda, B, ldb, V, ldv, VL, ldvl));
     int cur = 0;

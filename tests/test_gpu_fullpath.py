@@ -196,9 +196,11 @@ def test_two_chain_multicluster_stress(sdc):
     # configs[3] pencil recipe at n = 2304: both chains' stacks (4608 rows) take multi-cluster
     # panels at the same time; 64-row panel blocks ask for more clusters than half the GPU,
     # so the per-chain cap is exercised.  10 repeats: no barrier timeout, bit-identical.
+    # (SDC_CQ_SPLIT=0: by default two chains that share the SMs run these stack panels as split
+    # chains; the multi-cluster kernel stays the path of GRURV's tall panels at n > 4096.)
     from paper_1011_3077_b200 import inputs
     p = inputs.make_config(4, n=2304)
-    h = handle_env(sdc, 2304, pencil=True, SDC_PANEL_ROWS=64)
+    h = handle_env(sdc, 2304, pencil=True, SDC_PANEL_ROWS=64, SDC_CQ_SPLIT=0)
     A, B, V, VL = dev(p.A), dev(p.B), dev(p.V), dev(p.VL)
     outs = []
     for _ in range(10):
@@ -210,6 +212,21 @@ def test_two_chain_multicluster_stress(sdc):
         assert torch.equal(Q, outs[0][0]) and torch.equal(QL, outs[0][1])
         assert (r, met) == outs[0][2:]
     print("schedule counters:", c)
+
+
+def test_two_chain_default_takes_split_chains(sdc):
+    # default knobs: the same two-chain step runs its 4608-row stack panels as split chains
+    # (no cluster has to gather SMs between the other chain's CTAs); same result twice
+    from paper_1011_3077_b200 import inputs
+    p = inputs.make_config(4, n=2304)
+    h = sdc.Handle(2304, pencil=True)
+    A, B, V, VL = dev(p.A), dev(p.B), dev(p.V), dev(p.VL)
+    Q, QL, _, info = h.split(A, B, V, VL, max_iters=6)
+    c = h.schedule_counters()
+    assert c["panel_cq_split"] > 0 and c["cq_split_breakdowns"] == 0 and c["ctx_forks"] > 0, c
+    Q2, QL2, _, info2 = h.split(A, B, V, VL, max_iters=6)
+    assert torch.equal(Q, Q2) and torch.equal(QL, QL2) and info.metric == info2.metric
+    assert orth_err(host(Q)) <= 1e-13 * 2304 and orth_err(host(QL)) <= 1e-13 * 2304
 
 
 # ---- the split CholeskyQR2 panel chain (csrc/cqr_split.cuh) on the twins: at full size it is
