@@ -44,11 +44,12 @@ def test_batched_parity(orc, handle, n, batch, passes):
         i = infos[b]
         assert (i.k, i.r, i.status) == (o.k, o.r, o.status), b
         # converged steps: |dmetric| <= 1e-12 (north_star); a step still short of its floor
-        # after `passes` is rounding-sensitive and compared relatively (Q18)
+        # after `passes` is compared relatively: squaring doubles a relative perturbation per
+        # pass, so eps grows to at most 2^passes eps ~ 1e-7 (Q18)
         if o.metric <= 1e-11:
             assert abs(i.metric - o.metric) <= 1e-12
         else:
-            assert abs(i.metric - o.metric) <= 0.5 * o.metric
+            assert abs(i.metric - o.metric) <= 1e-4 * o.metric
         q = Qh[b].T
         assert orth_err(q) <= 1e-13 * n
         if o.status == 0:

@@ -92,4 +92,11 @@ def test_config4_full_pencil(api):
     idx = [(int(i), int(j)) for i, j in rng.integers(0, n, size=(6, 2))]
     scale = float(torch.linalg.norm(p.A, 1))
     assert sampled_similarity(p.A, QL, Q, Ah, idx) <= 1e-12 * scale * np.sqrt(n)
-    assert abs(info.k - n // 2) <= 4 * np.sqrt(n)   # spherical ensemble: half inside
+    # k pinned by an independent count: eigenvalues of B^{-1} A (torch, test side) inside the
+    # unit circle; an eigenvalue within 1e-6 of the circle may fall on either side of a rounding-
+    # level difference (kappa(B) ~ 1e4 amplifies eps), so it widens the pin by one
+    lam = torch.linalg.eigvals(torch.linalg.solve(p.B, p.A)).abs().cpu().numpy()
+    k_ref = int(np.sum(lam < 1.0))
+    margin = int(np.sum(np.abs(lam - 1.0) < 1e-6))
+    assert abs(info.k - k_ref) <= margin, (info.k, k_ref, margin)
+    assert margin <= 2
