@@ -64,3 +64,15 @@ def test_dmma_in_sass():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", build.LIB],
                          capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in out
+
+
+def test_schedule_counter_names_match_header():
+    # the binding's counter names (api.Handle.schedule_counters) follow the enum of include/sdc.h
+    import os
+    import re
+    from paper_1011_3077_b200 import _lib
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "sdc.h")).read()
+    enum = dict((m.group(1), int(m.group(2))) for m in re.finditer(r"SDC_SCHED_([A-Z0-9_]+) = (\d+)", hdr))
+    assert enum.pop("COUNTERS") == len(_lib.SCHED_NAMES) == len(enum)
+    for name, idx in enum.items():
+        assert _lib.SCHED_NAMES[idx].upper() == name, (name, idx, _lib.SCHED_NAMES[idx])
