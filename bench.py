@@ -346,6 +346,18 @@ def run_schur(args, rank, world, local):
             c = st_.counts
             return blocks, {"splits": int(c[0]), "failed_attempts": int(c[1]), "unsplit": int(c[2]),
                             "passes": int(c[3]), "max_metric": st_.max_metric}, Qd, Td
+    elif args.threads > 1:
+        # thread-ranks on this GPU: own handle and stream per rank, queue transport (parallel_schur.py)
+        from paper_1011_3077_b200 import parallel_schur as ps
+        handles = [h] + [api.Handle(n, device=local) for _ in range(args.threads - 1)]
+
+        def one():
+            torch.cuda.synchronize()
+            Qd, Td, blocks, st_ = ps.schur_threads(args.threads, lambda r: ps.GpuBackend(handles[r], **kw), A,
+                                                    device=local)
+            c = st_.counts
+            return blocks, {"splits": int(c[0]), "failed_attempts": int(c[1]), "unsplit": int(c[2]),
+                            "passes": int(c[3]), "max_metric": st_.max_metric}, Qd, Td
     else:
         def one():
             _, _, blocks, info = h.schur(A, Q=Q, T=T, **kw)
@@ -387,7 +399,9 @@ def run_schur(args, rank, world, local):
                                    f"(conjugate pairs, seed 88), n={n}, leaf {leaf}, seed 5, monitor tol 1e-13",
                        "n": n, "leaf": leaf,
                        "parallelism": (f"recursion over {world} ranks (smaller subproblem handed off per split)"
-                                       if world > 1 else "single"),
+                                       if world > 1 else
+                                       f"recursion over {args.threads} thread-ranks on one GPU (own handle each)"
+                                       if args.threads > 1 else "single"),
                        "l2": "working set (5 n^2 doubles) exceeds L2; no flush needed"},
             "result": {"blocks": len(blocks), "max_block": max(m for _, m in blocks), **info,
                        "residual_1": resid},
@@ -533,6 +547,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-n", type=int, default=1536)
+    ap.add_argument("--threads", type=int, default=1,
+                    help="config 8: thread-ranks on the one GPU (each with its own handle): the subtree handed "
+                         "off after a split runs concurrently on the same device")
     ap.add_argument("--leaf", type=int, default=64,
                     help="config 8: largest diagonal block left unsplit (1 = down to 1x1 / 2x2 blocks; blocks of "
                          "order <= 64 run in the batched kernel)")

@@ -208,3 +208,56 @@ def schur(be, comm, rank: int, world: int, A: torch.Tensor | None = None, n: int
     _send(comm, sub.Z, par)
     _send(comm, sub.T, par)
     return None
+
+
+# ---------------------------------------------------------------------------------------
+# Ranks as host threads on ONE GPU: each rank has its own handle (workspace, streams); the
+# subtrees handed off after a split then run concurrently on the same device -- their steps are
+# latency-bound chains at these sizes, so they overlap almost for free.  Whole blocks are
+# exchanged between kernels through queues (no kernel of one rank waits on another's kernel).
+# ---------------------------------------------------------------------------------------
+class ThreadComm:
+    """send/recv between threads of one process (rank = thread-local); tensors are copied on send."""
+
+    def __init__(self, world: int):
+        import queue
+        import threading
+        self.q = {(s, d): queue.Queue() for s in range(world) for d in range(world)}
+        self.local = threading.local()
+
+    def send(self, t, dst):
+        c = t.clone()
+        if c.is_cuda:   # the receiver copies on ITS stream: the clone must have completed
+            torch.cuda.current_stream(c.device).synchronize()
+        self.q[(self.local.rank, dst)].put(c)
+
+    def recv(self, t, src):
+        t.copy_(self.q[(src, self.local.rank)].get(timeout=3600))
+
+
+def schur_threads(world: int, make_backend, A: torch.Tensor, device: int = 0):
+    """One decomposition by `world` thread-ranks on `device`; make_backend(rank) -> backend with
+    its own handle.  Returns rank 0's (Q, T, blocks, stats)."""
+    import threading
+    comm = ThreadComm(world)
+    out, err = {}, []
+
+    def body(rank):
+        try:
+            comm.local.rank = rank
+            torch.cuda.set_device(device)
+            with torch.cuda.stream(torch.cuda.Stream(device=device)):
+                r = schur(make_backend(rank), comm, rank, world, A if rank == 0 else None)
+                torch.cuda.current_stream().synchronize()
+            out[rank] = r
+        except Exception as e:  # noqa: BLE001 -- surfaced to the caller below
+            err.append(e)
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return out[0]

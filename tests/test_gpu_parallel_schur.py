@@ -82,3 +82,28 @@ def test_gpu_multirank_schur_matches_one_rank(orc, world):
     assert np.linalg.norm(Qh @ Th @ Qh.T - A) <= 1e-12 * n * np.linalg.norm(A)
     o = orc.schur(A, **kw)
     assert blocks == o.blocks and st.counts[:3].tolist() == [o.splits, o.failed_attempts, o.unsplit]
+
+
+def test_gpu_thread_ranks_module_helper(orc):
+    # parallel_schur.schur_threads: 4 thread-ranks on the one GPU, each with its own handle AND
+    # its own stream (the product helper behind `bench.py --config 8 --threads 4`): the same
+    # block list, counters and diagonal blocks as one rank
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1011_3077_b200 import api, parallel_schur as ps
+    kw = dict(leaf=16, seed=5, max_iters=60, tol=1e-13)
+    n = 200
+    A, _, _ = inputs.normal_random_eigs(n, 41, 42)
+    Ad = torch.as_tensor(np.asfortranarray(A)).cuda().t().contiguous().t()
+    h = api.Handle(n)
+    Q1, T1, blocks1, info1 = h.schur(Ad, **kw)
+    handles = [api.Handle(n) for _ in range(4)]
+    Q, T, blocks, st = ps.schur_threads(4, lambda r: ps.GpuBackend(handles[r], **kw), Ad)
+    torch.cuda.synchronize()
+    assert blocks == blocks1
+    assert st.counts.tolist() == [info1["splits"], info1["failed_attempts"], info1["unsplit"], info1["passes"]]
+    Qh, Th, T1h = Q.cpu().numpy(), T.cpu().numpy(), T1.cpu().numpy()
+    for b0, m in blocks:
+        assert np.array_equal(Th[b0:b0 + m, b0:b0 + m], T1h[b0:b0 + m, b0:b0 + m])
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(Qh @ Th @ Qh.T - A) <= 1e-12 * n * np.linalg.norm(A)
