@@ -62,9 +62,11 @@ def run(n, knobs):
 
     t_cp = timed(cp)
     t_qr = timed(qr) - t_cp
-    h.profile(True)
+    noprof = bool(os.environ.get("STAGE_NOPROF"))   # per-class events off (they disable some schedules)
+    if not noprof:
+        h.profile(True)
     t_irs = timed(irs, reps=1)
-    prof = [h.profile_read(c) for c in range(7)]
+    prof = [h.profile_read(c) for c in range(7)] if not noprof else []
     h.profile(False)
     n3 = float(n) ** 3
     tf = lambda c, ms: c * n3 / (ms * 1e-3) / 1e12   # noqa: E731
