@@ -22,6 +22,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/sdc.h"
@@ -641,6 +642,7 @@ inline int rpt_slot(int rpt) { return rpt == 8 ? 1 : rpt == 16 ? 2 : rpt == 32 ?
 // dynamic shared memory currently allowed per (device, exchange mode, RPT variant) of the panel
 // kernel (the attribute is per device; sdc_create re-sets the cluster RPT=0 entry it probes)
 size_t g_panel_attr[MAX_DEV][2][4] = {};
+std::mutex g_panel_mu;   // the limits only grow, under this lock (handles on several host threads)
 
 // The CholeskyQR2 panel as six small kernels (cqr_split.cuh): wide, bandwidth-trivial stages
 // on m/256 CTAs and the serial 64 x 64 chains on one CTA, so a tall panel that runs next to the
@@ -724,15 +726,20 @@ int panel(sdc_handle* h, double* P, long long ldp, int m, int nb, double* Y, lon
   size_t smem = panel_smem_bytes(rows_per, h->cqr);
   const int rpt = h->panel_reg ? panel_rpt(rows_per) : 0;
   const void* fn = panel_fn(cluster, rpt);
-  size_t& cur = g_panel_attr[h->device & (MAX_DEV - 1)][cluster][rpt_slot(rpt)];
-  if (smem > cur) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) {
-      set_err("panel: %d rows per CTA need %zu B of shared memory (n too large): %s", rows_per,
-              smem, cudaGetErrorString(e));
-      return SDC_ERR_NOT_SUPPORTED;
+  {
+    // several handles may run on several host threads (thread-ranks of the recursion): the
+    // limit only ever grows, under a lock, so no thread lowers it below another's launch
+    std::lock_guard<std::mutex> lk(g_panel_mu);
+    size_t& cur = g_panel_attr[h->device & (MAX_DEV - 1)][cluster][rpt_slot(rpt)];
+    if (smem > cur) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        set_err("panel: %d rows per CTA need %zu B of shared memory (n too large): %s", rows_per,
+                smem, cudaGetErrorString(e));
+        return SDC_ERR_NOT_SUPPORTED;
+      }
+      cur = smem;
     }
-    cur = smem;
   }
   // CholeskyQR2 first (register variants in cluster mode, full-width panels), Householder on
   // breakdown (cqr.cuh)
@@ -1662,8 +1669,12 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
                                       1) == cudaSuccess;
     const void* fn16 = panel_fn(true, 0);
     if (np) {
-      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)panel_smem_bytes(cdiv(h->cluster_max_rows, 16), h->cqr));
+      // the occupancy probes need the limit >= their footprints; it is never lowered (another
+      // handle, possibly on another host thread, may be launching this variant)
+      std::lock_guard<std::mutex> lk(g_panel_mu);
+      size_t& cur0 = g_panel_attr[device & (MAX_DEV - 1)][1][rpt_slot(0)];
+      cur0 = std::max({cur0, panel_smem_bytes(cdiv(h->cluster_max_rows, 16), h->cqr), panel_smem_bytes(256, h->cqr)});
+      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cur0);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(16);
       cfg.blockDim = dim3(PANEL_THREADS);
@@ -1680,7 +1691,6 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
         h->cluster_ok = true;
       // tall panels: how many 16-CTA clusters with ~256-row blocks can be resident at once
       cfg.dynamicSmemBytes = panel_smem_bytes(256, h->cqr);
-      cudaFuncSetAttribute(fn16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)panel_smem_bytes(256, h->cqr));
       int ncl2 = 0;
       if (cudaOccupancyMaxActiveClusters(&ncl2, fn16, &cfg) == cudaSuccess && ncl2 >= 2) {
         h->max_clusters16 = ncl2;
@@ -1691,8 +1701,6 @@ int sdc_create(sdc_handle** out, int device, int n_max, int pencil) {
       cfg.gridDim = dim3(8);
       if (cudaOccupancyMaxActiveClusters(&ncl8, fn16, &cfg) == cudaSuccess) h->max_clusters8 = ncl8;
       cudaGetLastError();
-      // the probe above re-set this variant's limit: keep panel()'s per-device cache in step
-      g_panel_attr[device & (MAX_DEV - 1)][1][rpt_slot(0)] = panel_smem_bytes(256, h->cqr);
     }
     if (getenv("SDC_NO_CLUSTER")) h->cluster_ok = h->mcluster_ok = false;
     if (getenv("SDC_NO_MCLUSTER")) h->mcluster_ok = false;
